@@ -1,0 +1,148 @@
+/* tsg.h — C ABI of the B200-native streaming ST-HOSVD update.
+ *
+ * This is the drop-in boundary for the reference's streaming API
+ * (reference proj/include/tucker/streaming.hpp). The reference exposes C++
+ * only; each entry point below replaces one reference call and keeps its
+ * argument meaning, layouts and error behaviour:
+ *
+ *   tsg_init            <- tucker::stream_init               streaming.hpp:55
+ *   tsg_update          <- tucker::stream_update             streaming.hpp:63
+ *   tsg_process_mode    <- tucker::process_nonstreaming_mode streaming.hpp:69-70
+ *   tsg_estimate_relative_error
+ *                       <- tucker::estimate_relative_error   streaming.hpp:79
+ *   tsg_import_state    <- tucker::assemble_streaming_state  streaming.hpp:85-87
+ *   tsg_export_state    <- StreamingState fields + streaming_factor()
+ *                                                            streaming.hpp:34-49
+ *   tsg_metrics_at / tsg_last_metrics
+ *                       <- StreamingState::metrics (SliceMetrics, streaming.hpp:13-22)
+ *   tsg_sym_eig_desc, tsg_small_svd_truncated, tsg_mode_subspace, tsg_ttm
+ *                       <- linalg.hpp:42,54; sthosvd.hpp:38; tensor.hpp:66
+ *                          (device implementations; exposed for parity tests)
+ *
+ * Error behaviour: every function returns a status. TSG_EINVAL mirrors
+ * std::invalid_argument / std::out_of_range, TSG_EDRIFT mirrors the
+ * std::runtime_error thrown when the core / ISVD coupling drifts
+ * (streaming.cpp:39-64), TSG_EDEVICE reports a CUDA failure. The message is
+ * available from tsg_last_error(h) (or tsg_last_error(NULL) for handle-less
+ * calls).
+ *
+ * Layouts (identical to the reference): tensors colexicographic
+ * (mode 0 fastest); factor matrices column-major N_k x R_k; the core
+ * R_0 x ... x R_{d-1}; right (Q) column-major n x r, n = R_0...R_{d-2};
+ * the streaming factor ("left") exported column-major n_d x r as
+ * StreamingState::streaming_factor() returns it.
+ *
+ * Memory: TSG_MEM_HOST pointers are copied to the device inside the call;
+ * TSG_MEM_DEVICE pointers must be device-resident fp64 buffers that stay
+ * valid until the call returns (or until tsg_synchronize in async mode).
+ * The handle owns all device memory; one host thread drives a handle.
+ */
+#ifndef TSG_H
+#define TSG_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TSG_MAXD 8
+
+enum tsg_status {
+  TSG_OK = 0,
+  TSG_EINVAL = 1,   /* std::invalid_argument */
+  TSG_EDRIFT = 2,   /* coupling drift: std::runtime_error */
+  TSG_EOTHER = 3,
+  TSG_EDEVICE = 4   /* CUDA error */
+};
+
+enum tsg_mem_kind { TSG_MEM_HOST = 0, TSG_MEM_DEVICE = 1 };
+
+enum tsg_flags {
+  /* tsg_update returns once the work is enqueued; drift and device errors
+   * surface at the next call. Default: synchronous, like the reference. */
+  TSG_ASYNC = 1
+};
+
+typedef struct tsg_stream tsg_stream;
+
+typedef struct {
+  int32_t device;            /* CUDA ordinal */
+  int32_t flags;             /* tsg_flags */
+  int64_t rank_capacity;     /* initial streaming-rank capacity (0 = auto) */
+  int64_t row_capacity;      /* initial n_d capacity (0 = auto) */
+  int64_t reorthogonalize_every; /* ISVDOptions (isvd.hpp:62-67); must be 0 */
+} tsg_config;
+
+/* Same layout as oracle/oracle_abi.h orc_dims. */
+typedef struct {
+  int32_t order;
+  int64_t n_d;
+  int64_t rank;
+  int64_t insertions;
+  int64_t core_dims[TSG_MAXD];
+  int64_t slice_dims[TSG_MAXD];
+  double tau, squared_error, total_input_sq, nonstream_discarded_sq;
+} tsg_dims;
+
+/* SliceMetrics (streaming.hpp:13-22) plus parity diagnostics. */
+typedef struct {
+  int64_t slice_index;
+  int64_t ranks[TSG_MAXD];
+  double slice_norm, projected_norm, error_estimate;
+  double mode_residuals[TSG_MAXD];
+  int32_t expanded_mask;     /* bit k: mode k grew on this slice */
+  int64_t peak_bytes;        /* device high-water mark of this handle */
+  double wall_ms;            /* host wall time of the call */
+  double trunc_margin;       /* |trailing - delta^2| / delta^2 of the ISVD cut */
+  int32_t jacobi_sweeps;     /* inner-SVD sweeps */
+} tsg_slice_metrics;
+
+int tsg_create(const tsg_config* cfg, tsg_stream** out);
+void tsg_destroy(tsg_stream* h);
+const char* tsg_last_error(const tsg_stream* h);
+
+int tsg_init(tsg_stream* h, const double* x, int32_t order,
+             const int64_t* dims, double tau, int32_t mem_kind);
+int tsg_update(tsg_stream* h, const double* slice, int32_t mem_kind);
+int tsg_synchronize(tsg_stream* h);
+
+int tsg_process_mode(tsg_stream* h, const double* y, const int64_t* ydims,
+                     int32_t mode, double delta, double* y_out,
+                     int64_t y_out_cap, int64_t* ydims_out, double* res);
+
+int tsg_query(tsg_stream* h, tsg_dims* out);
+int tsg_export_state(tsg_stream* h, double* core, double* factors,
+                     double* sigma, double* left, double* right);
+int tsg_import_state(tsg_stream* h, const tsg_dims* dims, const double* core,
+                     const double* factors, const double* sigma,
+                     const double* left, const double* right);
+double tsg_estimate_relative_error(tsg_stream* h);
+
+int64_t tsg_metrics_count(tsg_stream* h);
+int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out);
+int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out);
+
+/* Number of kernels this handle has launched (for launch accounting). */
+int64_t tsg_kernel_launches(tsg_stream* h);
+/* The CUDA stream the handle enqueues on (cudaStream_t as void*). */
+void* tsg_cuda_stream(tsg_stream* h);
+/* Device pointer to an internal scratch slice buffer of slice size
+ * (for callers that synthesize slices on the device). */
+double* tsg_slice_buffer(tsg_stream* h, int32_t which);
+
+/* Device building blocks on host buffers (column-major). */
+int tsg_sym_eig_desc(int64_t n, const double* g, double* evals, double* evecs);
+int tsg_small_svd_truncated(int64_t m, int64_t n, const double* a, double thr,
+                            double* left, double* sigma, double* right,
+                            int64_t* rank, double* disc);
+int tsg_mode_subspace(const double* t, int32_t order, const int64_t* dims,
+                      int32_t mode, double delta, double* basis,
+                      int64_t* rank, double* evals, double* disc);
+int tsg_ttm(const double* t, int32_t order, const int64_t* dims, int32_t mode,
+            const double* a, int64_t a_rows, int64_t a_cols,
+            int32_t transpose_a, double* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TSG_H */

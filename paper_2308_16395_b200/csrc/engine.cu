@@ -1,0 +1,1212 @@
+// Host side of the B200 streaming ST-HOSVD engine and its C ABI (include/tsg.h).
+//
+// The handle owns the streaming state in HBM in the reference's layouts
+// (SURVEY A19): factors U_k (N_k x R_k, column-major, ld N_k, capacity N_k
+// columns), core and right factor Q as n x r slabs (core colexicographic
+// R_0 x .. x R_{d-2} x r == v_tensor's buffer, streaming.cpp:19-35), the
+// streaming factor ("left") row-major n_d x capr, and a device control block
+// holding ledgers, ranks and per-slice scalars. The steady-state update
+// (no basis growth) is enqueued with exactly one host synchronisation: after
+// the mode projections, to learn whether a non-streaming basis must grow.
+// Growth (rare) and stream_init run host-orchestrated on the same kernels.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tsg.h"
+#include "kernels.cuh"
+
+using namespace tsg;
+
+namespace {
+
+struct TsgError : std::runtime_error {
+  int code;
+  TsgError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw TsgError(code, msg); }
+
+void ck(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(TSG_EDEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+thread_local std::string g_free_err;
+
+long long prod(const long long* d, int n) {
+  long long p = 1;
+  for (int i = 0; i < n; ++i) p *= d[i];
+  return p;
+}
+
+}  // namespace
+
+struct tsg_stream {
+  int device = 0;
+  int flags = 0;
+  cudaStream_t st = nullptr;
+  std::string err;
+
+  // dims (host mirror; exact)
+  int d = 0;
+  double tau = 0.0;
+  long long N[kMaxD] = {0};
+  long long R[kMaxD] = {0};
+  long long n_d = 0;
+  long long insertions_host = 0;
+  int r_host = 0;  // streaming rank as of the last synchronisation
+  int capr = 0;
+  long long cap_rows = 0;
+  long long slice_elems = 0;
+  bool initialized = false;
+
+  // device state
+  double* U[kMaxD] = {nullptr};
+  double *core = nullptr, *core2 = nullptr, *Q = nullptr, *Q2 = nullptr;
+  long long qcap = 0;  // doubles per Q/core buffer
+  double *sigma = nullptr, *sigma2 = nullptr;
+  double *left = nullptr, *left2 = nullptr;
+  double* slice = nullptr;   // device staging for host slices
+  double* slice_b = nullptr; // second caller-visible slice buffer
+  double *w0 = nullptr, *w1 = nullptr;
+  double* ebuf = nullptr;
+  double* kbuf = nullptr;
+  double* evec = nullptr;
+  double* partial = nullptr;
+  long long partial_cap = 0;
+  double* ipart = nullptr;
+  long long ipart_cap = 0;
+  double* pgram = nullptr;
+  double* inner = nullptr;
+  Ctrl* ctrl = nullptr;
+  Ctrl* ctrl_h = nullptr;
+  Metrics* mdev = nullptr;
+  Metrics* mhost = nullptr;
+  int mslot = 0;
+  bool pending = false;       // an ISVD record not yet drained
+  int pending_slot = 0;
+  int pending_mask = 0;
+  double pending_wall = 0.0;
+  std::vector<tsg_slice_metrics> metrics;
+
+  long long cur_bytes = 0, peak_bytes = 0;
+  std::vector<std::pair<void*, long long>> allocs;
+  long long launches_at_create = 0;
+
+  // ------------------------------------------------------------ memory
+  double* dalloc(long long n_doubles) {
+    if (n_doubles <= 0) n_doubles = 1;
+    void* p = nullptr;
+    ck(cudaMalloc(&p, n_doubles * sizeof(double)), "cudaMalloc");
+    allocs.emplace_back(p, n_doubles * (long long)sizeof(double));
+    cur_bytes += n_doubles * (long long)sizeof(double);
+    peak_bytes = std::max(peak_bytes, cur_bytes);
+    return static_cast<double*>(p);
+  }
+  void dfree(void* p) {
+    if (!p) return;
+    for (size_t i = 0; i < allocs.size(); ++i)
+      if (allocs[i].first == p) {
+        cur_bytes -= allocs[i].second;
+        allocs.erase(allocs.begin() + i);
+        break;
+      }
+    cudaFree(p);
+  }
+  void free_all() {
+    for (auto& a : allocs) cudaFree(a.first);
+    allocs.clear();
+    cur_bytes = 0;
+    if (ctrl_h) cudaFreeHost(ctrl_h);
+    if (mhost) cudaFreeHost(mhost);
+    ctrl_h = nullptr;
+    mhost = nullptr;
+  }
+
+  void sync() { ck(cudaStreamSynchronize(st), "cudaStreamSynchronize"); }
+
+  void pull_ctrl() {
+    ck(cudaMemcpyAsync(ctrl_h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
+    sync();
+    ck(cudaGetLastError(), "kernel");
+  }
+  void push_ctrl() {
+    ck(cudaMemcpyAsync(ctrl, ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl H2D");
+  }
+
+  long long n_rows() const { return prod(R, d - 1); }
+
+  // --------------------------------------------------------- buffers
+  // Partials for every mode plus one spare region, allocated once so that
+  // pointers captured by enqueued kernels stay valid.
+  void ensure_partial(long long n) {
+    const long long need = std::max(n, 2LL * 148 * (kMaxD + 1) + 64);
+    if (need <= partial_cap) return;
+    if (partial) sync();
+    dfree(partial);
+    partial_cap = need;
+    partial = dalloc(partial_cap);
+  }
+  void ensure_isvd_buffers() {
+    // capr must leave room for r+1 columns after the insertion
+    const long long need_ip = (296LL * (capr + 1)) * 2 + 296 + 2 * 148 * 8 + 64;
+    if (need_ip > ipart_cap) {
+      dfree(ipart);
+      ipart_cap = need_ip;
+      ipart = dalloc(ipart_cap);
+    }
+  }
+  void grow_capr(int new_capr) {
+    // Q / core hold n x capr; left holds cap_rows x capr; sigma capr
+    const long long n = n_rows();
+    sync();
+    double* nq = dalloc(n * new_capr);
+    double* nc = dalloc(n * new_capr);
+    double* nq2 = dalloc(n * new_capr);
+    double* nc2 = dalloc(n * new_capr);
+    ck(cudaMemcpyAsync(nq, Q, sizeof(double) * n * capr, cudaMemcpyDeviceToDevice, st), "grow");
+    ck(cudaMemcpyAsync(nc, core, sizeof(double) * n * capr, cudaMemcpyDeviceToDevice, st), "grow");
+    double* nl = dalloc(cap_rows * new_capr);
+    double* nl2 = dalloc(cap_rows * new_capr);
+    ck(cudaMemset2DAsync(nl, new_capr * sizeof(double), 0, new_capr * sizeof(double), cap_rows, st), "memset");
+    ck(cudaMemcpy2DAsync(nl, new_capr * sizeof(double), left, capr * sizeof(double),
+                         capr * sizeof(double), cap_rows, cudaMemcpyDeviceToDevice, st), "grow left");
+    double* ns = dalloc(new_capr + 1);
+    double* ns2 = dalloc(new_capr + 1);
+    ck(cudaMemcpyAsync(ns, sigma, sizeof(double) * capr, cudaMemcpyDeviceToDevice, st), "grow");
+    double* npg = dalloc((long long)new_capr * new_capr);
+    double* nin = dalloc(isvd_inner_scratch(new_capr));
+    sync();
+    dfree(Q); dfree(Q2); dfree(core); dfree(core2); dfree(left); dfree(left2);
+    dfree(sigma); dfree(sigma2); dfree(pgram); dfree(inner);
+    Q = nq; Q2 = nq2; core = nc; core2 = nc2; left = nl; left2 = nl2;
+    sigma = ns; sigma2 = ns2; pgram = npg; inner = nin;
+    capr = new_capr;
+    qcap = n * new_capr;
+    ensure_isvd_buffers();
+  }
+  void grow_rows(long long need) {
+    if (need <= cap_rows) return;
+    long long nr = std::max(need, cap_rows * 2);
+    double* nl = dalloc(nr * capr);
+    double* nl2 = dalloc(nr * capr);
+    ck(cudaMemsetAsync(nl, 0, sizeof(double) * nr * capr, st), "memset");
+    ck(cudaMemcpyAsync(nl, left, sizeof(double) * cap_rows * capr, cudaMemcpyDeviceToDevice, st), "grow rows");
+    sync();
+    dfree(left); dfree(left2);
+    left = nl; left2 = nl2;
+    cap_rows = nr;
+  }
+
+  // ---------------------------------------------------- metrics drain
+  void drain() {
+    if (!pending) return;
+    ck(cudaMemcpyAsync(mhost + pending_slot, mdev + pending_slot, sizeof(Metrics),
+                       cudaMemcpyDeviceToHost, st), "metrics D2H");
+    sync();
+    const Metrics& m = mhost[pending_slot];
+    tsg_slice_metrics o;
+    std::memset(&o, 0, sizeof o);
+    o.slice_index = m.slice_index;
+    for (int k = 0; k < d; ++k) o.ranks[k] = m.ranks[k];
+    o.slice_norm = m.slice_norm;
+    o.projected_norm = m.projected_norm;
+    o.error_estimate = m.error_estimate;
+    for (int k = 0; k + 1 < d; ++k) o.mode_residuals[k] = m.mode_residuals[k];
+    o.expanded_mask = pending_mask;
+    o.peak_bytes = peak_bytes;
+    o.wall_ms = pending_wall;
+    o.trunc_margin = m.trunc_margin;
+    o.jacobi_sweeps = m.sweeps;
+    metrics.push_back(o);
+    pending = false;
+  }
+
+  void check_status() {
+    if (ctrl_h->status == 2)
+      fail(TSG_EDRIFT,
+           "streaming state invariant violated: core no longer matches the ISVD factorization");
+    if (ctrl_h->status != 0) fail(TSG_EOTHER, "device numerical failure");
+  }
+
+  // ---------------------------------------------------- mode subspace
+  struct Sub {
+    double* basis = nullptr;  // rows x rank (ld rows)
+    double* evals = nullptr;  // >= rows entries
+    long long rank = 0;
+    double disc = 0.0;
+    std::vector<double*> owned;
+  };
+  void release(Sub& s) {
+    for (double* p : s.owned) dfree(p);
+    s.owned.clear();
+  }
+
+  // mode_subspace (sthosvd.cpp:39-92) on a device tensor.
+  Sub mode_subspace(const double* t, const long long* dims, int order, int mode, double delta) {
+    Sub s;
+    const long long rows = dims[mode];
+    const long long size = prod(dims, order);
+    const long long cols = rows == 0 ? 0 : size / rows;
+    if (rows <= 0) fail(TSG_EINVAL, "mode_subspace: empty mode");
+    ModeView v{prod(dims, mode), rows, prod(dims + mode + 1, order - mode - 1)};
+    const double* A = t;
+    if (mode != 0) {
+      double* a = dalloc(size);
+      s.owned.push_back(a);
+      launch_unfold(t, v, a, st);
+      A = a;
+    }
+    long long* rk_d = reinterpret_cast<long long*>(dalloc(2));
+    s.owned.push_back(reinterpret_cast<double*>(rk_d));
+    double* disc_d = reinterpret_cast<double*>(rk_d) + 1;
+    if (rows <= cols) {
+      double* g = dalloc(rows * rows);
+      const int splits = gram_splits((int)rows, cols);
+      double* part = dalloc((long long)splits * rows * rows);
+      double* work = dalloc(2 * rows * rows);
+      double* vec = dalloc(rows * rows);
+      double* ev = dalloc(rows);
+      s.owned.insert(s.owned.end(), {g, part, work, vec, ev});
+      launch_gram(A, (int)rows, cols, g, part, st);
+      launch_sym_eig(g, (int)rows, ev, vec, work, nullptr, st);
+      launch_truncate(ev, (int)rows, delta, 0, rk_d, disc_d, st);
+      long long hr[2];
+      ck(cudaMemcpyAsync(hr, rk_d, 16, cudaMemcpyDeviceToHost, st), "rank D2H");
+      sync();
+      ck(cudaGetLastError(), "mode_subspace");
+      s.rank = hr[0];
+      std::memcpy(&s.disc, &hr[1], 8);
+      s.basis = vec;
+      s.evals = ev;
+      return s;
+    }
+    // thin route
+    double* g = dalloc(cols * cols);
+    double* work = dalloc(2 * cols * cols);
+    double* vec = dalloc(cols * cols);
+    double* ev = dalloc(rows);
+    s.owned.insert(s.owned.end(), {g, work, vec, ev});
+    ck(cudaMemsetAsync(ev, 0, sizeof(double) * rows, st), "memset");
+    launch_gram_t(A, rows, (int)cols, g, st);
+    launch_sym_eig(g, (int)cols, ev, vec, work, nullptr, st);
+    launch_truncate(ev, (int)cols, delta, 1, rk_d, disc_d, st);
+    long long hr[2];
+    ck(cudaMemcpyAsync(hr, rk_d, 16, cudaMemcpyDeviceToHost, st), "rank D2H");
+    sync();
+    ck(cudaGetLastError(), "mode_subspace");
+    s.rank = hr[0];
+    std::memcpy(&s.disc, &hr[1], 8);
+    double* basis = dalloc(rows * std::max(s.rank, 1LL));
+    s.owned.push_back(basis);
+    launch_gemm_nn(A, rows, vec, cols, basis, rows, rows, (int)s.rank, (int)cols, st);
+    launch_scale_cols_invsqrt(basis, rows, rows, (int)s.rank, ev, st);
+    launch_mgs(basis, rows, rows, (int)s.rank, st);
+    s.basis = basis;
+    s.evals = ev;
+    return s;
+  }
+
+  // ------------------------------------------------------- projection
+  // Projection of y (dims yd, order d-1) along `mode`: P into out,
+  // partials into `part`; returns partial count.
+  int project(const double* y, const long long* yd, int mode, double* out, double* part,
+              double* e = nullptr) {
+    ProjArgs a;
+    a.x = y;
+    a.v = ModeView{prod(yd, mode), yd[mode], prod(yd + mode + 1, d - 2 - mode)};
+    a.u = U[mode];
+    a.R = (int)R[mode];
+    a.p = out;
+    a.e = e;
+    a.partial = part;
+    a.residual = 1;
+    return launch_project(a, st);
+  }
+
+  // Grow U_k by the residual's dominant directions (streaming.cpp:142-151).
+  // y: mode input tensor (dims yd); p: its projection; result written to
+  // `dst` (concat of p and the carried coefficients), yd updated.
+  void expand_mode(const double* y, long long* yd, int mode, double delta, const double* p,
+                   double* dst) {
+    if (!ebuf) ebuf = dalloc(slice_elems);
+    if (!kbuf) kbuf = dalloc(slice_elems);
+    ModeView v{prod(yd, mode), yd[mode], prod(yd + mode + 1, d - 2 - mode)};
+    project(y, yd, mode, nullptr, partial + 2LL * 148 * kMaxD, ebuf);
+    Sub s = mode_subspace(ebuf, yd, d - 1, mode, delta);
+    const long long g = s.rank;
+    if (R[mode] + g > N[mode]) fail(TSG_EOTHER, "expansion exceeds the mode size");
+    // carried = W^T E (streaming.cpp:145)
+    ProjArgs a;
+    a.x = ebuf;
+    a.v = v;
+    a.u = s.basis;
+    a.R = (int)g;
+    a.p = kbuf;
+    a.e = nullptr;
+    a.partial = nullptr;
+    a.residual = 0;
+    launch_project(a, st);
+    // U_k <- [U_k W] (old columns untouched)
+    ck(cudaMemcpyAsync(U[mode] + R[mode] * N[mode], s.basis, sizeof(double) * N[mode] * g,
+                       cudaMemcpyDeviceToDevice, st), "hcat");
+    // pad core and v (= Q) along mode (tensor.cpp:168-184)
+    long long cd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) cd[k] = R[k];
+    const int r = ctrl_h->r;
+    cd[d - 1] = r;
+    ModeView cv{prod(cd, mode), R[mode], prod(cd + mode + 1, d - 1 - mode)};
+    const long long n_new = n_rows() / R[mode] * (R[mode] + g);
+    const long long new_qcap = n_new * capr;
+    double* nq = dalloc(new_qcap);
+    double* nc = dalloc(new_qcap);
+    launch_pad(Q, cv, g, nq, st);
+    launch_pad(core, cv, g, nc, st);
+    double* nq2 = dalloc(new_qcap);
+    double* nc2 = dalloc(new_qcap);
+    // ledger (streaming.cpp:150)
+    double* dd = dalloc(1);
+    ck(cudaMemcpyAsync(dd, &s.disc, 8, cudaMemcpyHostToDevice, st), "disc");
+    launch_ledger_add_nonstream(ctrl, dd, st);
+    // y <- concat_k(P, carried)
+    launch_concat(p, kbuf, v.left, R[mode], g, v.right, dst, st);
+    sync();
+    dfree(dd);
+    dfree(Q); dfree(Q2); dfree(core); dfree(core2);
+    Q = nq; Q2 = nq2; core = nc; core2 = nc2;
+    qcap = new_qcap;
+    if (e_alloc_n() < n_new) {
+      dfree(evec);
+      evec = dalloc(n_new);
+      evec_n = n_new;
+    }
+    release(s);
+    R[mode] += g;
+    yd[mode] = R[mode];
+  }
+  long long evec_n = 0;
+  long long e_alloc_n() const { return evec_n; }
+
+  // ---------------------------------------------------------- update
+  void update(const double* y_in, int mem_kind) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
+    const double* y = y_in;
+    if (mem_kind == TSG_MEM_HOST) {
+      ck(cudaMemcpyAsync(slice, y_in, sizeof(double) * slice_elems, cudaMemcpyHostToDevice, st),
+         "slice H2D");
+      y = slice;
+    }
+    // speculative projections of every non-streaming mode
+    long long yd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+    DecideArgs da;
+    std::memset(&da, 0, sizeof da);
+    da.ctrl = ctrl;
+    da.nmodes = d - 1;
+    da.tau = tau;
+    da.order = d;
+    ensure_partial(2LL * 148 * (d - 1) + 16);
+    const double* in[kMaxD];
+    double* outb[kMaxD];
+    const double* cur = y;
+    int off = 0;
+    for (int k = 0; k + 1 < d; ++k) {
+      double* out = (cur == w0) ? w1 : w0;
+      in[k] = cur;
+      outb[k] = out;
+      da.off[k] = off;
+      da.cnt[k] = project(cur, yd, k, out, partial + off);
+      off += 2 * da.cnt[k];
+      yd[k] = R[k];
+      cur = out;
+    }
+    da.partial = partial;
+    da.first_mode = 0;
+    launch_decide(da, st);
+    drain_async_pending();
+    pull_ctrl();
+    check_status();
+    r_host = ctrl_h->r;
+    int mask = 0;
+    if (ctrl_h->zero_slice) {
+      launch_commit_modes(ctrl, 0, 0, 1, st);
+      grow_rows(n_d + 1);
+      long long sp[kMaxD] = {0};
+      for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
+      launch_zero_slice(ctrl, left, capr, mdev + mslot, d, sp, st);
+      ++n_d;
+      finish(t0, 0);
+      return;
+    }
+    int em = ctrl_h->expand_mode;
+    if (em < 0) {
+      launch_commit_modes(ctrl, 0, d - 1, 1, st);
+    } else {
+      launch_commit_modes(ctrl, 0, em, 1, st);
+      const double delta = ctrl_h->delta;
+      // dims of the tensor entering mode em
+      long long ydm[kMaxD];
+      for (int k = 0; k + 1 < d; ++k) ydm[k] = (k < em) ? R[k] : N[k];
+      int k = em;
+      const double* yk = in[em];
+      while (true) {
+        // the other work buffer receives the concatenation
+        double* dst = (outb[k] == w0) ? w1 : w0;
+        if (dst == yk && yk != y) {
+          // yk is one of the work buffers and dst aliases it: safe, yk is
+          // no longer needed once E and the carried block are formed.
+        }
+        if (dst == y) dst = (outb[k] == w0) ? w1 : w0;
+        expand_mode(yk, ydm, k, delta, outb[k], dst);
+        mask |= 1 << k;
+        cur = dst;
+        if (k + 1 >= d - 1) break;
+        // re-project the remaining modes on the grown tensor
+        DecideArgs db = da;
+        int off2 = 0;
+        const double* c2 = dst;
+        for (int kk = k + 1; kk + 1 < d; ++kk) {
+          double* out = (c2 == w0) ? w1 : w0;
+          in[kk] = c2;
+          outb[kk] = out;
+          db.off[kk] = off2;
+          db.cnt[kk] = project(c2, ydm, kk, out, partial + off2);
+          off2 += 2 * db.cnt[kk];
+          ydm[kk] = R[kk];
+          c2 = out;
+        }
+        db.first_mode = k + 1;
+        launch_decide(db, st);
+        pull_ctrl();
+        const int em2 = ctrl_h->expand_mode;
+        cur = c2;
+        if (em2 < 0) {
+          launch_commit_modes(ctrl, k + 1, d - 1, 0, st);
+          break;
+        }
+        launch_commit_modes(ctrl, k + 1, em2, 0, st);
+        for (int kk = em2 + 1; kk + 1 < d; ++kk) ydm[kk] = N[kk];
+        k = em2;
+        yk = in[k];
+      }
+    }
+    // ----- ISVD row insertion + core rotation (isvd.cpp:163-250, streaming.cpp:196-224)
+    const int r = ctrl_h->r;
+    if (r + 1 > capr) grow_capr(std::max(capr + 16, (r + 1 + 7) / 8 * 8 + 8));
+    grow_rows(n_d + 1);
+    const long long n = n_rows();
+    if (evec_n < n) {
+      dfree(evec);
+      evec = dalloc(n);
+      evec_n = n;
+    }
+    IsvdBufs B;
+    std::memset(&B, 0, sizeof B);
+    B.ctrl = ctrl;
+    B.b = cur;
+    B.q = Q;
+    B.qn = Q2;
+    B.c = core;
+    B.cn = core2;
+    B.e = evec;
+    B.sigma = sigma;
+    B.sigma_new = sigma2;
+    B.left = left;
+    B.left_new = left2;
+    B.pgram = pgram;
+    B.inner = inner;
+    B.partial = ipart;
+    B.metrics = mdev + mslot;
+    B.n = n;
+    B.n_d = n_d;
+    B.capr = capr;
+    B.order = d;
+    for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
+    launch_isvd(B, st);
+    std::swap(Q, Q2);
+    std::swap(core, core2);
+    std::swap(sigma, sigma2);
+    std::swap(left, left2);
+    ++n_d;
+    ++insertions_host;
+    finish(t0, mask);
+  }
+
+  void finish(std::chrono::steady_clock::time_point t0, int mask) {
+    pending = true;
+    pending_slot = mslot;
+    pending_mask = mask;
+    mslot ^= 1;
+    if (!(flags & TSG_ASYNC)) {
+      pull_ctrl();
+      r_host = ctrl_h->r;
+      pending_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      drain();
+      check_status();
+    } else {
+      pending_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+  }
+  // In async mode the previous record is complete once this slice's
+  // projections are (same stream); fetch it with the ctrl block.
+  void drain_async_pending() {
+    if (pending) drain();
+  }
+
+  void flush() {
+    drain();
+    pull_ctrl();
+    r_host = ctrl_h->r;
+    check_status();
+  }
+
+  // ------------------------------------------------------------ init
+  void init(const double* x, int order, const long long* dims, double t, int mem_kind) {
+    if (order < 2) fail(TSG_EINVAL, "stream_init: need at least one non-streaming mode");
+    if (order > kMaxD) fail(TSG_EINVAL, "stream_init: order exceeds TSG_MAXD");
+    for (int k = 0; k < order; ++k)
+      if (dims[k] <= 0) fail(TSG_EINVAL, "stream_init: dims must be positive");
+    reset_state();
+    d = order;
+    tau = t;
+    const long long size = prod(dims, order);
+    double* X = dalloc(size);
+    ck(cudaMemcpyAsync(X, x, sizeof(double) * size,
+                       mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                       st), "init H2D");
+    double* nrm = dalloc(1 + 1024);
+    launch_sumsq(X, size, nrm, nrm + 1, st);
+    double xsq = 0.0;
+    ck(cudaMemcpyAsync(&xsq, nrm, 8, cudaMemcpyDeviceToHost, st), "norm D2H");
+    sync();
+    ck(cudaGetLastError(), "init norm");
+    dfree(nrm);
+    if (std::sqrt(xsq) == 0.0) {
+      dfree(X);
+      fail(TSG_EINVAL, "stream_init: initial batch must be nonzero to seed a factorization");
+    }
+    if (!(t > 0.0 && t < 1.0)) {
+      dfree(X);
+      fail(TSG_EINVAL, "sthosvd: tau must lie in (0, 1)");
+    }
+    // sthosvd (sthosvd.cpp:94-133)
+    const double delta = t * std::sqrt(xsq) / std::sqrt((double)order);
+    long long cd[kMaxD];
+    for (int k = 0; k < order; ++k) cd[k] = dims[k];
+    double* coreT = X;
+    double discarded = 0.0;
+    Sub last;
+    double* left_cm = nullptr;
+    for (int k = 0; k < order; ++k) {
+      Sub s = mode_subspace(coreT, cd, order, k, delta);
+      const long long rk = s.rank;
+      ModeView v{prod(cd, k), cd[k], prod(cd + k + 1, order - k - 1)};
+      double* nc = dalloc(v.left * rk * v.right);
+      ProjArgs a;
+      a.x = coreT;
+      a.v = v;
+      a.u = s.basis;
+      a.R = (int)rk;
+      a.p = nc;
+      a.e = nullptr;
+      a.partial = nullptr;
+      a.residual = 0;
+      launch_project(a, st);
+      if (k < order - 1) {
+        N[k] = dims[k];
+        R[k] = rk;
+        U[k] = dalloc(N[k] * N[k]);
+        ck(cudaMemcpyAsync(U[k], s.basis, sizeof(double) * N[k] * rk, cudaMemcpyDeviceToDevice, st),
+           "factor");
+      } else {
+        left_cm = dalloc(dims[k] * rk);
+        ck(cudaMemcpyAsync(left_cm, s.basis, sizeof(double) * dims[k] * rk,
+                           cudaMemcpyDeviceToDevice, st), "left");
+      }
+      discarded += s.disc;
+      sync();
+      if (coreT != X) dfree(coreT);
+      else dfree(X);
+      coreT = nc;
+      cd[k] = rk;
+      if (k == order - 1) {
+        last = s;
+      } else {
+        release(s);
+      }
+    }
+    const int r = (int)cd[order - 1];
+    const long long n = prod(cd, order - 1);
+    n_d = dims[order - 1];
+    slice_elems = prod(dims, order - 1);
+    capr = std::max(16, (2 * r + 8 + 7) / 8 * 8);
+    if (cfg_capr > 0) capr = std::max<int>(capr, (int)cfg_capr);
+    cap_rows = std::max<long long>(cfg_rows > 0 ? cfg_rows : 0, std::max(256LL, 2 * n_d));
+    qcap = n * capr;
+    Q = dalloc(qcap);
+    Q2 = dalloc(qcap);
+    core = dalloc(qcap);
+    core2 = dalloc(qcap);
+    sigma = dalloc(capr + 1);
+    sigma2 = dalloc(capr + 1);
+    left = dalloc(cap_rows * capr);
+    left2 = dalloc(cap_rows * capr);
+    ck(cudaMemsetAsync(left, 0, sizeof(double) * cap_rows * capr, st), "memset");
+    pgram = dalloc((long long)capr * capr);
+    inner = dalloc(isvd_inner_scratch(capr));
+    slice = dalloc(slice_elems);
+    slice_b = dalloc(slice_elems);
+    w0 = dalloc(slice_elems);
+    w1 = dalloc(slice_elems);
+    evec = dalloc(n);
+    evec_n = n;
+    ensure_isvd_buffers();
+    ensure_partial(0);
+    ck(cudaMemcpyAsync(core, coreT, sizeof(double) * n * r, cudaMemcpyDeviceToDevice, st), "core");
+    launch_init_isvd(ctrl, coreT, n, r, last.evals, Q, sigma, left_cm, n_d, left, capr, st);
+    // isvd_init validation (isvd.cpp:139-153)
+    double* od = dalloc(2);
+    launch_orth_defect(left_cm, n_d, n_d, r, od, st);
+    launch_orth_defect(Q, n, n, r, od + 1, st);
+    std::memset(ctrl_h, 0, sizeof(Ctrl));
+    ctrl_h->squared_error = discarded;
+    ctrl_h->total_input_sq = xsq;
+    ctrl_h->nonstream_discarded_sq = 0.0;
+    ctrl_h->r = r;
+    ctrl_h->n_d = n_d;
+    ctrl_h->expand_mode = -1;
+    push_ctrl();
+    launch_coupling_check(ctrl, core, Q, sigma, n, r, nullptr, st);
+    double defects[2];
+    std::vector<double> sv(r);
+    ck(cudaMemcpyAsync(defects, od, 16, cudaMemcpyDeviceToHost, st), "defect");
+    ck(cudaMemcpyAsync(sv.data(), sigma, 8 * r, cudaMemcpyDeviceToHost, st), "sigma");
+    pull_ctrl();
+    dfree(od);
+    dfree(coreT);
+    dfree(left_cm);
+    release(last);
+    for (int k = order - 1; k < kMaxD; ++k) R[k] = 0;
+    r_host = r;
+    if (defects[0] > 1e-6) fail(TSG_EINVAL, "isvd_init: left factor not orthonormal");
+    if (defects[1] > 1e-6) fail(TSG_EINVAL, "isvd_init: right factor not orthonormal");
+    for (int j = 0; j < r; ++j) {
+      if (!(sv[j] > 0.0)) fail(TSG_EINVAL, "isvd_init: singular values must be positive");
+      if (j > 0 && sv[j] > sv[j - 1]) fail(TSG_EINVAL, "isvd_init: singular values must descend");
+    }
+    if (!(discarded >= 0.0)) fail(TSG_EINVAL, "isvd_init: initial squared error must be nonnegative");
+    check_status();
+    initialized = true;
+  }
+
+  long long cfg_capr = 0, cfg_rows = 0;
+
+  void reset_state() {
+    free_all();
+    for (int k = 0; k < kMaxD; ++k) U[k] = nullptr;
+    core = core2 = Q = Q2 = sigma = sigma2 = left = left2 = nullptr;
+    slice = slice_b = w0 = w1 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
+    partial_cap = ipart_cap = 0;
+    evec_n = 0;
+    metrics.clear();
+    pending = false;
+    mslot = 0;
+    initialized = false;
+    n_d = 0;
+    insertions_host = 0;
+    ctrl = reinterpret_cast<Ctrl*>(dalloc((sizeof(Ctrl) + 7) / 8));
+    ck(cudaMallocHost(&ctrl_h, sizeof(Ctrl)), "cudaMallocHost");
+    std::memset(ctrl_h, 0, sizeof(Ctrl));
+    push_ctrl();
+    mdev = reinterpret_cast<Metrics*>(dalloc(2 * ((sizeof(Metrics) + 7) / 8)));
+    ck(cudaMallocHost(&mhost, 2 * sizeof(Metrics)), "cudaMallocHost");
+  }
+
+  // ------------------------------------------------------ export/import
+  void query(tsg_dims* o) {
+    flush();
+    std::memset(o, 0, sizeof *o);
+    o->order = d;
+    o->n_d = ctrl_h->n_d;
+    o->rank = ctrl_h->r;
+    o->insertions = ctrl_h->insertions;
+    for (int k = 0; k + 1 < d; ++k) {
+      o->core_dims[k] = R[k];
+      o->slice_dims[k] = N[k];
+    }
+    o->core_dims[d - 1] = ctrl_h->r;
+    o->tau = tau;
+    o->squared_error = ctrl_h->squared_error;
+    o->total_input_sq = ctrl_h->total_input_sq;
+    o->nonstream_discarded_sq = ctrl_h->nonstream_discarded_sq;
+  }
+
+  void export_state(double* hcore, double* factors, double* hsigma, double* hleft, double* hright) {
+    flush();
+    const int r = ctrl_h->r;
+    const long long n = n_rows();
+    const long long nd = ctrl_h->n_d;
+    if (hcore) ck(cudaMemcpy(hcore, core, sizeof(double) * n * r, cudaMemcpyDeviceToHost), "export");
+    if (hright) ck(cudaMemcpy(hright, Q, sizeof(double) * n * r, cudaMemcpyDeviceToHost), "export");
+    if (hsigma) ck(cudaMemcpy(hsigma, sigma, sizeof(double) * r, cudaMemcpyDeviceToHost), "export");
+    if (factors) {
+      long long off = 0;
+      for (int k = 0; k + 1 < d; ++k) {
+        ck(cudaMemcpy(factors + off, U[k], sizeof(double) * N[k] * R[k], cudaMemcpyDeviceToHost),
+           "export");
+        off += N[k] * R[k];
+      }
+    }
+    if (hleft) {
+      std::vector<double> rm(std::max<long long>(nd * capr, 1));
+      ck(cudaMemcpy(rm.data(), left, sizeof(double) * nd * capr, cudaMemcpyDeviceToHost), "export");
+      for (long long i = 0; i < nd; ++i)
+        for (int j = 0; j < r; ++j) hleft[i + j * nd] = rm[i * capr + j];
+    }
+  }
+
+  void import_state(const tsg_dims* dm, const double* hcore, const double* factors,
+                    const double* hsigma, const double* hleft, const double* hright) {
+    const int order = dm->order;
+    if (order < 2 || order > kMaxD) fail(TSG_EINVAL, "assemble_streaming_state: need d >= 2");
+    reset_state();
+    d = order;
+    tau = dm->tau;
+    for (int k = 0; k + 1 < d; ++k) {
+      N[k] = dm->slice_dims[k];
+      R[k] = dm->core_dims[k];
+      if (R[k] > N[k] || R[k] <= 0) fail(TSG_EINVAL, "assemble_streaming_state: bad ranks");
+    }
+    const int r = (int)dm->core_dims[d - 1];
+    const long long n = n_rows();
+    n_d = dm->n_d;
+    slice_elems = prod(N, d - 1);
+    capr = std::max(16, (2 * r + 8 + 7) / 8 * 8);
+    cap_rows = std::max(256LL, 2 * n_d);
+    qcap = n * capr;
+    Q = dalloc(qcap); Q2 = dalloc(qcap); core = dalloc(qcap); core2 = dalloc(qcap);
+    sigma = dalloc(capr + 1); sigma2 = dalloc(capr + 1);
+    left = dalloc(cap_rows * capr); left2 = dalloc(cap_rows * capr);
+    pgram = dalloc((long long)capr * capr);
+    inner = dalloc(isvd_inner_scratch(capr));
+    slice = dalloc(slice_elems); slice_b = dalloc(slice_elems);
+    w0 = dalloc(slice_elems); w1 = dalloc(slice_elems);
+    evec = dalloc(n);
+    evec_n = n;
+    ensure_isvd_buffers();
+    ensure_partial(0);
+    long long off = 0;
+    for (int k = 0; k + 1 < d; ++k) {
+      U[k] = dalloc(N[k] * N[k]);
+      ck(cudaMemcpy(U[k], factors + off, sizeof(double) * N[k] * R[k], cudaMemcpyHostToDevice), "import");
+      off += N[k] * R[k];
+    }
+    ck(cudaMemcpy(core, hcore, sizeof(double) * n * r, cudaMemcpyHostToDevice), "import");
+    ck(cudaMemcpy(Q, hright, sizeof(double) * n * r, cudaMemcpyHostToDevice), "import");
+    ck(cudaMemcpy(sigma, hsigma, sizeof(double) * r, cudaMemcpyHostToDevice), "import");
+    std::vector<double> rm(cap_rows * capr, 0.0);
+    for (long long i = 0; i < n_d; ++i)
+      for (int j = 0; j < r; ++j) rm[i * capr + j] = hleft[i + j * n_d];
+    ck(cudaMemcpy(left, rm.data(), sizeof(double) * cap_rows * capr, cudaMemcpyHostToDevice), "import");
+    std::memset(ctrl_h, 0, sizeof(Ctrl));
+    ctrl_h->squared_error = dm->squared_error;
+    ctrl_h->total_input_sq = dm->total_input_sq;
+    ctrl_h->nonstream_discarded_sq = dm->nonstream_discarded_sq;
+    ctrl_h->r = r;
+    ctrl_h->n_d = n_d;
+    ctrl_h->insertions = dm->insertions;
+    ctrl_h->expand_mode = -1;
+    push_ctrl();
+    launch_coupling_check(ctrl, core, Q, sigma, n, r, nullptr, st);
+    pull_ctrl();
+    r_host = r;
+    check_status();
+    initialized = true;
+  }
+
+  // process_nonstreaming_mode (streaming.cpp:126-155) on a host tensor.
+  double process_mode(const double* y_h, const long long* ydims, int mode, double delta,
+                      double* y_out, long long cap, long long* ydims_out) {
+    if (mode < 0 || mode >= d - 1) fail(TSG_EINVAL, "process_mode: mode out of range");
+    if (ydims[mode] != N[mode]) fail(TSG_EINVAL, "process_mode: shape mismatch");
+    flush();
+    long long yd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = ydims[k];
+    const long long size = prod(yd, d - 1);
+    double* yb = dalloc(size);
+    double* pb = dalloc(size);
+    double* cb = dalloc(size + prod(yd, d - 1) / std::max(1LL, yd[mode]) * N[mode]);
+    ck(cudaMemcpyAsync(yb, y_h, sizeof(double) * size, cudaMemcpyHostToDevice, st), "y H2D");
+    ensure_partial(2 * 148 + 16);
+    DecideArgs da;
+    std::memset(&da, 0, sizeof da);
+    da.ctrl = ctrl;
+    da.nmodes = mode + 1;
+    da.tau = tau;
+    da.order = d;
+    da.partial = partial;
+    da.off[mode] = 0;
+    da.cnt[mode] = project(yb, yd, mode, pb, partial);
+    da.first_mode = mode;
+    // decide() computes delta only for first_mode == 0; set it explicitly
+    ctrl_h->delta = delta;
+    ck(cudaMemcpyAsync(&ctrl->delta, &delta, 8, cudaMemcpyHostToDevice, st), "delta");
+    launch_decide(da, st);
+    pull_ctrl();
+    const double res = std::sqrt(ctrl_h->res_sq[mode]);
+    const double* out = pb;
+    if (ctrl_h->expand_mode < 0) {
+      launch_commit_modes(ctrl, mode, mode + 1, 0, st);
+      yd[mode] = R[mode];
+    } else {
+      // sized for yd[mode] <= N[mode]
+      if (!ebuf || slice_elems < size) {
+        if (size > slice_elems) fail(TSG_EINVAL, "process_mode: tensor larger than a slice");
+      }
+      expand_mode(yb, yd, mode, delta, pb, cb);
+      out = cb;
+    }
+    const long long osz = prod(yd, d - 1);
+    if (osz > cap) fail(TSG_EINVAL, "process_mode: output capacity");
+    ck(cudaMemcpyAsync(y_out, out, sizeof(double) * osz, cudaMemcpyDeviceToHost, st), "y D2H");
+    sync();
+    for (int k = 0; k + 1 < d; ++k) ydims_out[k] = yd[k];
+    dfree(yb);
+    dfree(pb);
+    dfree(cb);
+    pull_ctrl();
+    return res;
+  }
+};
+
+// ===================================================================== C ABI
+namespace {
+
+template <class F>
+int guarded(tsg_stream* h, F&& f) {
+  try {
+    if (h) ck(cudaSetDevice(h->device), "cudaSetDevice");
+    f();
+    return TSG_OK;
+  } catch (const TsgError& e) {
+    (h ? h->err : g_free_err) = e.what();
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    (h ? h->err : g_free_err) = "host allocation failed";
+    return TSG_EOTHER;
+  } catch (const std::exception& e) {
+    (h ? h->err : g_free_err) = e.what();
+    return TSG_EOTHER;
+  }
+}
+
+// A scratch handle for the handle-less building blocks.
+struct Scratch {
+  cudaStream_t st = nullptr;
+  std::vector<void*> ptrs;
+  Scratch() { ck(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream"); }
+  ~Scratch() {
+    for (void* p : ptrs) cudaFree(p);
+    if (st) cudaStreamDestroy(st);
+  }
+  double* alloc(long long n) {
+    void* p = nullptr;
+    ck(cudaMalloc(&p, sizeof(double) * std::max(1LL, n)), "cudaMalloc");
+    ptrs.push_back(p);
+    return static_cast<double*>(p);
+  }
+  double* up(const double* h, long long n) {
+    double* p = alloc(n);
+    ck(cudaMemcpyAsync(p, h, sizeof(double) * n, cudaMemcpyHostToDevice, st), "H2D");
+    return p;
+  }
+  void down(double* h, const double* p, long long n) {
+    ck(cudaMemcpyAsync(h, p, sizeof(double) * n, cudaMemcpyDeviceToHost, st), "D2H");
+  }
+  void sync() {
+    ck(cudaStreamSynchronize(st), "sync");
+    ck(cudaGetLastError(), "kernel");
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int tsg_create(const tsg_config* cfg, tsg_stream** out) {
+  *out = nullptr;
+  tsg_stream* h = new (std::nothrow) tsg_stream();
+  if (!h) return TSG_EOTHER;
+  if (cfg) {
+    h->device = cfg->device;
+    h->flags = cfg->flags;
+    h->cfg_capr = cfg->rank_capacity;
+    h->cfg_rows = cfg->row_capacity;
+    if (cfg->reorthogonalize_every != 0) {
+      g_free_err = "reorthogonalize_every > 0 is not supported (reference default is 0)";
+      delete h;
+      return TSG_EINVAL;
+    }
+  }
+  int st = guarded(h, [&] {
+    int n = 0;
+    ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    if (h->device < 0 || h->device >= n) fail(TSG_EDEVICE, "no such CUDA device");
+    ck(cudaSetDevice(h->device), "cudaSetDevice");
+    ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "cudaStreamCreate");
+    h->launches_at_create = g_launches;
+  });
+  if (st) {
+    g_free_err = h->err;
+    delete h;
+    return st;
+  }
+  *out = h;
+  return TSG_OK;
+}
+
+void tsg_destroy(tsg_stream* h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  if (h->st) cudaStreamSynchronize(h->st);
+  h->free_all();
+  if (h->st) cudaStreamDestroy(h->st);
+  delete h;
+}
+
+const char* tsg_last_error(const tsg_stream* h) { return h ? h->err.c_str() : g_free_err.c_str(); }
+
+int tsg_init(tsg_stream* h, const double* x, int32_t order, const int64_t* dims, double tau,
+             int32_t mem_kind) {
+  return guarded(h, [&] {
+    long long dd[kMaxD];
+    if (order > kMaxD || order < 0) fail(TSG_EINVAL, "stream_init: bad order");
+    for (int k = 0; k < order; ++k) dd[k] = dims[k];
+    h->init(x, order, dd, tau, mem_kind);
+  });
+}
+
+int tsg_update(tsg_stream* h, const double* slice, int32_t mem_kind) {
+  return guarded(h, [&] { h->update(slice, mem_kind); });
+}
+
+int tsg_synchronize(tsg_stream* h) {
+  return guarded(h, [&] {
+    if (h->initialized) h->flush();
+    else h->sync();
+  });
+}
+
+int tsg_process_mode(tsg_stream* h, const double* y, const int64_t* ydims, int32_t mode,
+                     double delta, double* y_out, int64_t y_out_cap, int64_t* ydims_out,
+                     double* res) {
+  return guarded(h, [&] {
+    long long yd[kMaxD], od[kMaxD];
+    for (int k = 0; k + 1 < h->d; ++k) yd[k] = ydims[k];
+    *res = h->process_mode(y, yd, mode, delta, y_out, y_out_cap, od);
+    for (int k = 0; k + 1 < h->d; ++k) ydims_out[k] = od[k];
+  });
+}
+
+int tsg_query(tsg_stream* h, tsg_dims* out) {
+  return guarded(h, [&] {
+    if (!h->initialized) fail(TSG_EINVAL, "state not initialised");
+    h->query(out);
+  });
+}
+
+int tsg_export_state(tsg_stream* h, double* core, double* factors, double* sigma, double* left,
+                     double* right) {
+  return guarded(h, [&] {
+    if (!h->initialized) fail(TSG_EINVAL, "state not initialised");
+    h->export_state(core, factors, sigma, left, right);
+  });
+}
+
+int tsg_import_state(tsg_stream* h, const tsg_dims* dims, const double* core,
+                     const double* factors, const double* sigma, const double* left,
+                     const double* right) {
+  return guarded(h, [&] { h->import_state(dims, core, factors, sigma, left, right); });
+}
+
+double tsg_estimate_relative_error(tsg_stream* h) {
+  double out = 0.0;
+  guarded(h, [&] {
+    h->flush();
+    const Ctrl& c = *h->ctrl_h;
+    if (c.total_input_sq <= 0.0) return;
+    out = std::sqrt(std::max(c.squared_error + c.nonstream_discarded_sq, 0.0) / c.total_input_sq);
+  });
+  return out;
+}
+
+int64_t tsg_metrics_count(tsg_stream* h) {
+  int64_t n = -1;
+  guarded(h, [&] {
+    h->drain();
+    n = (int64_t)h->metrics.size();
+  });
+  return n;
+}
+
+int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out) {
+  return guarded(h, [&] {
+    h->drain();
+    if (i < 0 || i >= (int64_t)h->metrics.size()) fail(TSG_EINVAL, "metrics index out of range");
+    *out = h->metrics[(size_t)i];
+  });
+}
+
+int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out) {
+  return guarded(h, [&] {
+    h->drain();
+    if (h->metrics.empty()) fail(TSG_EINVAL, "no metrics recorded");
+    *out = h->metrics.back();
+  });
+}
+
+int64_t tsg_kernel_launches(tsg_stream* h) { return h ? g_launches - h->launches_at_create : g_launches; }
+
+void* tsg_cuda_stream(tsg_stream* h) { return h ? (void*)h->st : nullptr; }
+
+double* tsg_slice_buffer(tsg_stream* h, int32_t which) {
+  if (!h || !h->initialized) return nullptr;
+  return which ? h->slice_b : h->slice;
+}
+
+int tsg_sym_eig_desc(int64_t n, const double* g, double* evals, double* evecs) {
+  return guarded(nullptr, [&] {
+    double max_abs = 0.0, max_asym = 0.0;
+    for (int64_t j = 0; j < n; ++j)
+      for (int64_t i = 0; i < n; ++i) {
+        max_abs = std::max(max_abs, std::fabs(g[i + j * n]));
+        max_asym = std::max(max_asym, std::fabs(g[i + j * n] - g[j + i * n]));
+      }
+    if (max_asym > 1e-10 * std::max(max_abs, 1e-300))
+      fail(TSG_EINVAL, "sym_eig_desc: matrix is not symmetric");
+    if (n == 0) return;
+    Scratch s;
+    double* dg = s.up(g, n * n);
+    double* ev = s.alloc(n);
+    double* vec = s.alloc(n * n);
+    double* work = s.alloc(2 * n * n);
+    launch_sym_eig(dg, (int)n, ev, vec, work, nullptr, s.st);
+    s.down(evals, ev, n);
+    s.down(evecs, vec, n * n);
+    s.sync();
+  });
+}
+
+int tsg_small_svd_truncated(int64_t m, int64_t n, const double* a, double thr, double* left,
+                            double* sigma, double* right, int64_t* rank, double* disc) {
+  // small_svd_truncated (linalg.cpp:210-259) from the device building blocks
+  return guarded(nullptr, [&] {
+    if (thr < 0.0) fail(TSG_EINVAL, "small_svd_truncated: threshold must be nonnegative");
+    *rank = 0;
+    *disc = 0.0;
+    if (m == 0 || n == 0) return;
+    Scratch s;
+    double* da = s.up(a, m * n);
+    double* g = s.alloc(n * n);
+    double* ev = s.alloc(n);
+    double* vec = s.alloc(n * n);
+    double* work = s.alloc(2 * n * n);
+    double* rk = s.alloc(2);
+    launch_gram_t(da, m, (int)n, g, s.st);
+    launch_sym_eig(g, (int)n, ev, vec, work, nullptr, s.st);
+    double lam0 = 0.0;
+    s.down(&lam0, ev, 1);
+    s.sync();
+    if (std::sqrt(lam0) == 0.0) return;
+    launch_truncate(ev, (int)n, thr, 1, reinterpret_cast<long long*>(rk), rk + 1, s.st);
+    long long hr[2];
+    ck(cudaMemcpyAsync(hr, rk, 16, cudaMemcpyDeviceToHost, s.st), "D2H");
+    s.sync();
+    const long long r = hr[0];
+    std::memcpy(disc, &hr[1], 8);
+    *rank = r;
+    double* lf = s.alloc(m * r);
+    launch_gemm_nn(da, m, vec, n, lf, m, m, (int)r, (int)n, s.st);
+    launch_scale_cols_invsqrt(lf, m, m, (int)r, ev, s.st);
+    launch_mgs(lf, m, m, (int)r, s.st);
+    std::vector<double> lam(r);
+    s.down(lam.data(), ev, r);
+    s.down(right, vec, n * r);
+    s.down(left, lf, m * r);
+    s.sync();
+    for (long long j = 0; j < r; ++j) sigma[j] = std::sqrt(lam[j]);
+  });
+}
+
+int tsg_mode_subspace(const double* t, int32_t order, const int64_t* dims, int32_t mode,
+                      double delta, double* basis, int64_t* rank, double* evals, double* disc) {
+  tsg_stream tmp;
+  return guarded(nullptr, [&] {
+    ck(cudaStreamCreateWithFlags(&tmp.st, cudaStreamNonBlocking), "stream");
+    long long dd[kMaxD];
+    for (int k = 0; k < order; ++k) dd[k] = dims[k];
+    const long long size = prod(dd, order);
+    double* dt = tmp.dalloc(size);
+    ck(cudaMemcpy(dt, t, sizeof(double) * size, cudaMemcpyHostToDevice), "H2D");
+    auto s = tmp.mode_subspace(dt, dd, order, mode, delta);
+    *rank = s.rank;
+    *disc = s.disc;
+    const long long rows = dd[mode];
+    ck(cudaMemcpy(basis, s.basis, sizeof(double) * rows * s.rank, cudaMemcpyDeviceToHost), "D2H");
+    ck(cudaMemcpy(evals, s.evals, sizeof(double) * rows, cudaMemcpyDeviceToHost), "D2H");
+    tmp.release(s);
+    tmp.free_all();
+    cudaStreamDestroy(tmp.st);
+    tmp.st = nullptr;
+  });
+}
+
+int tsg_ttm(const double* t, int32_t order, const int64_t* dims, int32_t mode, const double* a,
+            int64_t a_rows, int64_t a_cols, int32_t transpose_a, double* out) {
+  return guarded(nullptr, [&] {
+    long long dd[kMaxD];
+    for (int k = 0; k < order; ++k) dd[k] = dims[k];
+    const long long contracted = transpose_a ? a_rows : a_cols;
+    if (mode < 0 || mode >= order) fail(TSG_EINVAL, "mode index out of range for tensor order");
+    if (contracted != dd[mode]) fail(TSG_EINVAL, "ttm: matrix does not match mode size");
+    const long long produced = transpose_a ? a_cols : a_rows;
+    Scratch s;
+    const long long size = prod(dd, order);
+    double* dt = s.up(t, size);
+    // P = U^T X with U = a (transpose_a) or a^T materialised
+    std::vector<double> u(a_rows * a_cols);
+    if (transpose_a) {
+      std::memcpy(u.data(), a, sizeof(double) * a_rows * a_cols);
+    } else {
+      for (long long i = 0; i < a_rows; ++i)
+        for (long long j = 0; j < a_cols; ++j) u[j + i * a_cols] = a[i + j * a_rows];
+    }
+    double* du = s.up(u.data(), a_rows * a_cols);
+    const long long osz = size / std::max(1LL, dd[mode]) * produced;
+    double* dout = s.alloc(osz);
+    ProjArgs pa;
+    pa.x = dt;
+    pa.v = ModeView{prod(dd, mode), dd[mode], prod(dd + mode + 1, order - mode - 1)};
+    pa.u = du;
+    pa.R = (int)produced;
+    pa.p = dout;
+    pa.e = nullptr;
+    pa.partial = nullptr;
+    pa.residual = 0;
+    if (osz > 0 && size > 0) launch_project(pa, s.st);
+    s.down(out, dout, osz);
+    s.sync();
+  });
+}
+
+}  // extern "C"

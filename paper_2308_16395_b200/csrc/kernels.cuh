@@ -1,0 +1,142 @@
+// Kernel launch interface of the B200 streaming ST-HOSVD engine.
+// All launches are asynchronous on the given stream; every launcher bumps
+// the launch counter so bench.py can report gpu_launches.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace tsg {
+
+extern long long g_launches;  // per-process launch counter (engine copies it per handle)
+
+// ---------------------------------------------------------------- linalg
+// Jacobi eigendecomposition of a symmetric n x n matrix (column-major, ld n)
+// in global memory, one CTA. Outputs eigenvalues (descending, clamped >= 0)
+// and eigenvectors (sign rule) exactly as sym_eig_desc (linalg.cpp:120-181)
+// specifies, with the cyclic sweep replaced by the round-robin parallel
+// ordering (every pair once per sweep). `work` holds 2 n*n doubles.
+void launch_sym_eig(const double* g, int n, double* evals, double* evecs,
+                    double* work, int* sweeps_out, cudaStream_t st);
+
+// Truncation of a descending spectrum (linalg.cpp:183-208, sthosvd.cpp:31-35):
+// optionally zero sqrt(l) <= 1e-14 sqrt(l_max) first (thin route).
+// out_rank[0] = rank, out_disc[0] = trailing sum.
+void launch_truncate(double* evals, int n, double delta, int zero_floor,
+                     long long* out_rank, double* out_disc, cudaStream_t st);
+
+// G = A A^T (rows x rows) for column-major A (rows x cols), exactly symmetric.
+// `partial` must hold splits*rows*rows doubles (see gram_splits()).
+int gram_splits(int rows, long long cols);
+void launch_gram(const double* a, int rows, long long cols, double* g,
+                 double* partial, cudaStream_t st);
+// G = A^T A (cols x cols), A column-major rows x cols.
+void launch_gram_t(const double* a, long long rows, int cols, double* g,
+                   cudaStream_t st);
+// C (m x n) = A (m x k, lda) * B (k x n, ldb), all column-major, plain FP64.
+void launch_gemm_nn(const double* a, long long lda, const double* b, long long ldb,
+                    double* c, long long ldc, long long m, int n, int k, cudaStream_t st);
+// Scale column j of A (m x n, lda) by 1/sqrt(evals[j]) (thin-route basis).
+void launch_scale_cols_invsqrt(double* a, long long lda, long long m, int n,
+                               const double* evals, cudaStream_t st);
+// One in-place modified Gram-Schmidt pass (linalg.cpp:64-78), right-looking.
+void launch_mgs(double* a, long long lda, long long m, int n, cudaStream_t st);
+// max |A^T A - I| (matrix.cpp:118-131) into out[0].
+void launch_orth_defect(const double* a, long long lda, long long m, int n,
+                        double* out, cudaStream_t st);
+
+// ------------------------------------------------------------- tensors
+// Mode-k view of a colexicographic tensor: (left, n, right).
+struct ModeView {
+  long long left, n, right;
+};
+// A[i + c n] = T[l + i left + r left n], c = l + r left (tensor.cpp:67-84).
+void launch_unfold(const double* t, ModeView v, double* a, cudaStream_t st);
+// Zero-pad along the mode: (left, n, right) -> (left, n + extra, right).
+void launch_pad(const double* t, ModeView v, long long extra, double* out,
+                cudaStream_t st);
+// Concatenate (left, na, right) and (left, nb, right) along the mode.
+void launch_concat(const double* a, const double* b, long long left,
+                   long long na, long long nb, long long right, double* out,
+                   cudaStream_t st);
+
+// Fused mode-k projection: P = U^T X_(k), optional residual
+// E = X - U P with per-CTA partials of ||E||^2 and ||X||^2.
+struct ProjArgs {
+  const double* x;
+  ModeView v;
+  const double* u;   // n x R, column-major, ld = v.n
+  int R;
+  double* p;         // (left, R, right) or nullptr
+  double* e;         // (left, n, right) or nullptr
+  double* partial;   // [grid * 2] (res_sq, x_sq) or nullptr
+  int residual;
+};
+// Returns the grid size (number of partial pairs written).
+int launch_project(const ProjArgs& a, cudaStream_t st);
+
+// Sum of squares of a device vector into out[0] (two-stage, deterministic).
+void launch_sumsq(const double* x, long long n, double* out, double* scratch,
+                  cudaStream_t st);
+
+// --------------------------------------------------------- streaming step
+struct DecideArgs {
+  Ctrl* ctrl;
+  const double* partial;     // concatenated partial pairs
+  int off[kMaxD], cnt[kMaxD];
+  int nmodes;                // d-1
+  int first_mode;            // first mode evaluated by this decide call
+  double tau;
+  int order;
+};
+void launch_decide(const DecideArgs& a, cudaStream_t st);
+// Ledger commit for modes [m0, m1): nonstream += ||E_k||^2 as rn*rn;
+// with_total adds slice_norm^2 to total_input_sq (streaming.cpp:168-169).
+void launch_commit_modes(Ctrl* ctrl, int m0, int m1, int with_total,
+                         cudaStream_t st);
+void launch_ledger_add_nonstream(Ctrl* ctrl, const double* value, cudaStream_t st);
+
+struct SpatialRanks {
+  long long v[kMaxD];
+};
+
+struct IsvdBufs {
+  Ctrl* ctrl;
+  const double* b;     // projected slice, length n
+  const double* q;     // n x r (ld n)
+  double* qn;          // n x r' out (ld n)
+  const double* c;     // core n x r (ld n)
+  double* cn;          // core out
+  double* e;           // length n scratch
+  const double* sigma; // r
+  double* sigma_new;   // r'
+  const double* left;  // n_d x r row-major, ld capr
+  double* left_new;
+  double* pgram;       // capr*capr
+  double* inner;       // scratch for the inner SVD (see engine)
+  double* partial;     // per-CTA partials
+  Metrics* metrics;    // record slot for this slice
+  long long n;
+  long long n_d;       // rows of left before the insertion
+  int capr;
+  int order;
+  long long spatial_ranks[kMaxD];
+};
+void launch_isvd(const IsvdBufs& b, cudaStream_t st);
+int isvd_inner_scratch(int capr);
+
+// Zero slice (streaming.cpp:171-185).
+void launch_zero_slice(Ctrl* ctrl, double* left, int capr, Metrics* rec,
+                       int order, const long long* spatial, cudaStream_t st);
+
+// stream_init helpers
+void launch_init_isvd(Ctrl* ctrl, const double* core, long long n, int r,
+                      const double* evals_last, double* q, double* sigma,
+                      const double* left_cm, long long n_init, double* left_rm,
+                      int capr, cudaStream_t st);
+void launch_coupling_check(Ctrl* ctrl, const double* core, const double* q,
+                           const double* sigma, long long n, int r,
+                           double* partial, cudaStream_t st);
+
+}  // namespace tsg

@@ -1,0 +1,594 @@
+// Dense linear algebra kernels of the B200 streaming ST-HOSVD engine:
+// Jacobi eigensolver, truncation rule, Gram (SYRK) kernels, MGS and the
+// tensor relayouts used by basis expansion and stream_init.
+//
+// Reference behaviour followed (paths relative to /root/reference/proj):
+//   sym_eig_desc          src/linalg.cpp:120-181 (rotation :27-60)
+//   truncation_rank       src/linalg.cpp:183-208
+//   gram_from_cols        src/linalg.cpp:80-94
+//   gram_transposed       src/linalg.cpp:100-114
+//   orthonormalize_columns src/linalg.cpp:64-78
+//   orthonormality_defect src/matrix.cpp:118-131
+//   unfold / pad / concat src/tensor.cpp:67-84, 168-209
+#include <cfloat>
+
+#include "kernels.cuh"
+
+namespace tsg {
+
+long long g_launches = 0;
+
+namespace {
+
+struct Rot {
+  double c, s, t;
+  int p, q;
+};
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// One CTA runs the whole eigensolve: sweeps of (np-1) rounds, each round
+// rotating np/2 disjoint pairs at once (round-robin "circle" ordering) so
+// every off-diagonal pair is annihilated once per sweep, as in the
+// reference's cyclic sweep. Stopping rule, rotation formulas, stable sort,
+// clamp and sign rule are the reference's (linalg.cpp:27-60,136-178).
+__device__ __forceinline__ int jacobi_sweeps(double* G, double* V, int n,
+                                             double tol, Rot* rot,
+                                             double* red) {
+  const int np = n + (n & 1);
+  const int half = np / 2;
+  const int rounds = np - 1;
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    double acc = 0.0;
+    for (long long idx = threadIdx.x; idx < (long long)n * n; idx += blockDim.x) {
+      const int i = (int)(idx % n), j = (int)(idx / n);
+      if (i != j) {
+        const double g = G[idx];
+        acc += g * g;
+      }
+    }
+    const double off = sqrt(block_sum(acc, red));
+    if (off <= tol || n < 2) break;
+    for (int rd = 0; rd < rounds; ++rd) {
+      for (int m = threadIdx.x; m < half; m += blockDim.x) {
+        int a, b;
+        if (m == 0) {
+          a = rd % (np - 1);
+          b = np - 1;
+        } else {
+          a = (rd + m) % (np - 1);
+          b = (rd + np - 1 - m) % (np - 1);
+        }
+        Rot R;
+        R.p = min(a, b);
+        R.q = max(a, b);
+        R.c = 1.0;
+        R.s = 0.0;
+        R.t = 0.0;
+        if (R.q < n) {
+          const double gpq = G[R.p + (long long)R.q * n];
+          if (gpq != 0.0) {
+            const double gpp = G[R.p + (long long)R.p * n];
+            const double gqq = G[R.q + (long long)R.q * n];
+            const double theta = (gqq - gpp) / (2.0 * gpq);
+            const double t = (theta >= 0.0)
+                                 ? 1.0 / (theta + sqrt(1.0 + theta * theta))
+                                 : 1.0 / (theta - sqrt(1.0 + theta * theta));
+            const double c = 1.0 / sqrt(1.0 + t * t);
+            R.c = c;
+            R.s = t * c;
+            R.t = t;
+          }
+        }
+        rot[m] = R;
+      }
+      __syncthreads();
+      const long long nblk = (long long)half * half;
+      for (long long bi = threadIdx.x; bi < nblk; bi += blockDim.x) {
+        const int m1 = (int)(bi / half), m2 = (int)(bi % half);
+        if (m1 > m2) continue;
+        const Rot A = rot[m1];
+        const Rot B = rot[m2];
+        const bool idA = (A.s == 0.0 && A.t == 0.0);
+        const bool idB = (B.s == 0.0 && B.t == 0.0);
+        if (idA && idB) continue;
+        const int p1 = A.p, q1 = A.q, p2 = B.p, q2 = B.q;
+        const bool q1v = q1 < n, q2v = q2 < n;
+        if (m1 == m2) {
+          // the rotated pair itself (linalg.cpp:50-53)
+          const double gpq = G[p1 + (long long)q1 * n];
+          const double gpp = G[p1 + (long long)p1 * n];
+          const double gqq = G[q1 + (long long)q1 * n];
+          G[p1 + (long long)p1 * n] = gpp - A.t * gpq;
+          G[q1 + (long long)q1 * n] = gqq + A.t * gpq;
+          G[p1 + (long long)q1 * n] = 0.0;
+          G[q1 + (long long)p1 * n] = 0.0;
+          continue;
+        }
+        // 2x2 block rows {p1,q1} x cols {p2,q2}: B' = J1^T B J2 (linalg.cpp:40-49)
+        const double b00 = G[p1 + (long long)p2 * n];
+        const double b01 = q2v ? G[p1 + (long long)q2 * n] : 0.0;
+        const double b10 = q1v ? G[q1 + (long long)p2 * n] : 0.0;
+        const double b11 = (q1v && q2v) ? G[q1 + (long long)q2 * n] : 0.0;
+        const double t00 = A.c * b00 - A.s * b10;
+        const double t01 = A.c * b01 - A.s * b11;
+        const double t10 = A.s * b00 + A.c * b10;
+        const double t11 = A.s * b01 + A.c * b11;
+        const double o00 = B.c * t00 - B.s * t01;
+        const double o01 = B.s * t00 + B.c * t01;
+        const double o10 = B.c * t10 - B.s * t11;
+        const double o11 = B.s * t10 + B.c * t11;
+        G[p1 + (long long)p2 * n] = o00;
+        G[p2 + (long long)p1 * n] = o00;
+        if (q2v) {
+          G[p1 + (long long)q2 * n] = o01;
+          G[q2 + (long long)p1 * n] = o01;
+        }
+        if (q1v) {
+          G[q1 + (long long)p2 * n] = o10;
+          G[p2 + (long long)q1 * n] = o10;
+        }
+        if (q1v && q2v) {
+          G[q1 + (long long)q2 * n] = o11;
+          G[q2 + (long long)q1 * n] = o11;
+        }
+      }
+      for (long long idx = threadIdx.x; idx < (long long)n * half; idx += blockDim.x) {
+        const int i = (int)(idx % n), m = (int)(idx / n);
+        const Rot R = rot[m];
+        if (R.q >= n || (R.s == 0.0 && R.t == 0.0)) continue;
+        const double vp = V[i + (long long)R.p * n], vq = V[i + (long long)R.q * n];
+        V[i + (long long)R.p * n] = R.c * vp - R.s * vq;
+        V[i + (long long)R.q * n] = R.s * vp + R.c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  return sweep;
+}
+
+// Stable descending sort of diag(G), clamp, copy columns with the sign rule.
+__device__ __forceinline__ void jacobi_finish(const double* G, const double* V,
+                                              int n, double* evals,
+                                              double* evecs, int* perm) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double di = G[i + (long long)i * n];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = G[j + (long long)j * n];
+      if (dj > di || (dj == di && j < i)) ++rank;
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < n; j += nw) {
+    const int src = perm[j];
+    double lambda = G[src + (long long)src * n];
+    if (lambda < 0.0) lambda = 0.0;
+    if (lane == 0) evals[j] = lambda;
+    // argmax |v| with first index on ties
+    double best = -1.0;
+    int arg = 0x7fffffff;
+    for (int i = lane; i < n; i += 32) {
+      const double a = fabs(V[i + (long long)src * n]);
+      if (a > best) {
+        best = a;
+        arg = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) {
+        best = ob;
+        arg = oa;
+      }
+    }
+    const double pivot = V[arg + (long long)src * n];
+    const bool flip = pivot < 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double v = V[i + (long long)src * n];
+      evecs[i + (long long)j * n] = flip ? -v : v;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(1024) sym_eig_kernel(const double* __restrict__ gin, int n,
+                                                       double* evals, double* evecs,
+                                                       double* work, int* sweeps_out) {
+  extern __shared__ unsigned char smem_raw[];
+  Rot* rot = reinterpret_cast<Rot*>(smem_raw);
+  int* perm = reinterpret_cast<int*>(rot + (n + 2) / 2);
+  __shared__ double red[32];
+  double* G = work;
+  double* V = work + (long long)n * n;
+  double acc = 0.0;
+  for (long long idx = threadIdx.x; idx < (long long)n * n; idx += blockDim.x) {
+    const double g = gin[idx];
+    G[idx] = g;
+    V[idx] = ((idx % n) == (idx / n)) ? 1.0 : 0.0;
+    acc += g * g;
+  }
+  const double tol = kOffDiagTolFactor * sqrt(block_sum(acc, red));
+  const int sw = jacobi_sweeps(G, V, n, tol, rot, red);
+  __syncthreads();
+  jacobi_finish(G, V, n, evals, evecs, perm);
+  if (threadIdx.x == 0 && sweeps_out) *sweeps_out = sw;
+}
+
+__global__ void truncate_kernel(double* ev, int n, double delta, int zero_floor,
+                                long long* out_rank, double* out_disc) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  if (n == 0) {
+    *out_rank = 0;
+    *out_disc = 0.0;
+    return;
+  }
+  if (zero_floor) {  // sthosvd.cpp:68-71, linalg.cpp:230-234
+    const double smax = sqrt(ev[0]);
+    const double fl = kSigmaZeroFactor * smax;
+    for (int i = 0; i < n; ++i)
+      if (sqrt(ev[i]) <= fl) ev[i] = 0.0;
+  }
+  const double budget = delta * delta;
+  // trailing[r] = trailing[r+1] + ev[r], accumulated from the tail; the
+  // admissible r form a suffix, so walk down while the budget holds.
+  double s = 0.0;
+  int r = n;
+
+  for (int i = n - 1; i >= 0; --i) {
+    const double next = s + ev[i];
+    if (next <= budget) {
+      s = next;
+      r = i;
+
+    } else {
+      break;
+    }
+  }
+  const int rank = r < 1 ? 1 : r;
+  double disc = 0.0;
+  for (int j = n - 1; j >= rank; --j) disc += ev[j];
+
+  *out_rank = rank;
+  *out_disc = disc;
+}
+
+// ---- Gram (SYRK) over a column-major rows x cols matrix, split over cols.
+constexpr int GT = 64;  // tile
+constexpr int GK = 16;  // k chunk
+
+__global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restrict__ a, int rows,
+                                                           long long cols, long long chunk,
+                                                           double* __restrict__ partial) {
+  const int nt = (rows + GT - 1) / GT;
+  // upper-triangular tile index -> (ti, tj), ti <= tj
+  int t = blockIdx.x, ti = 0;
+  while (t >= nt - ti) {
+    t -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const long long c0 = (long long)blockIdx.y * chunk;
+  const long long c1 = min(cols, c0 + chunk);
+  __shared__ double As[GK][GT + 1];
+  __shared__ double Bs[GK][GT + 1];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int i0 = ti * GT, j0 = tj * GT;
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+  for (long long cc = c0; cc < c1; cc += GK) {
+    for (int e = threadIdx.x; e < GT * GK; e += 256) {
+      const int ii = e % GT, kk = e / GT;
+      const long long c = cc + kk;
+      const int i = i0 + ii, j = j0 + ii;
+      As[kk][ii] = (i < rows && c < c1) ? a[i + c * rows] : 0.0;
+      Bs[kk][ii] = (j < rows && c < c1) ? a[j + c * rows] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; ++kk) {
+      double av[4], bv[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) av[x] = As[kk][ty + 16 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bv[y] = Bs[kk][tx + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] += av[x] * bv[y];
+    }
+    __syncthreads();
+  }
+  double* out = partial + (long long)blockIdx.y * rows * rows;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = i0 + ty + 16 * x, j = j0 + tx + 16 * y;
+      if (i < rows && j < rows) out[i + (long long)j * rows] = acc[x][y];
+    }
+}
+
+__global__ void gram_reduce_kernel(const double* __restrict__ partial, int rows, int splits,
+                                   double* __restrict__ g) {
+  const long long total = (long long)rows * rows;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int i = (int)(idx % rows), j = (int)(idx / rows);
+    if (i > j) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    double s = 0.0;
+    for (int sp = 0; sp < splits; ++sp) s += partial[(long long)sp * total + i + (long long)j * rows];
+    g[idx] = s;
+  }
+}
+
+__global__ void gram_t_kernel(const double* __restrict__ a, long long rows, int cols,
+                              double* __restrict__ g) {
+  const long long total = (long long)cols * cols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(idx % cols), j = (int)(idx / cols);
+    if (i > j) continue;
+    const double* ai = a + (long long)i * rows;
+    const double* aj = a + (long long)j * rows;
+    double dot = 0.0;
+    for (long long l = 0; l < rows; ++l) dot += ai[l] * aj[l];
+    g[i + (long long)j * cols] = dot;
+    g[j + (long long)i * cols] = dot;
+  }
+}
+
+__global__ void gemm_nn_kernel(const double* __restrict__ a, long long lda,
+                               const double* __restrict__ b, long long ldb, double* __restrict__ c,
+                               long long ldc, long long m, int n, int k) {
+  const long long total = m * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx % m;
+    const int j = (int)(idx / m);
+    double s = 0.0;
+    for (int l = 0; l < k; ++l) {
+      const double blj = b[l + j * ldb];
+      if (blj == 0.0) continue;  // matrix.cpp:44-52 skips zero multipliers
+      s += a[i + l * lda] * blj;
+    }
+    c[i + j * ldc] = s;
+  }
+}
+
+__global__ void scale_cols_invsqrt_kernel(double* a, long long lda, long long m, int n,
+                                          const double* __restrict__ ev) {
+  const long long total = m * n;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx % m;
+    const int j = (int)(idx / m);
+    const double inv = 1.0 / sqrt(ev[j]);
+    a[i + j * lda] *= inv;
+  }
+}
+
+__global__ void __launch_bounds__(1024) mgs_kernel(double* a, long long lda, long long m, int n) {
+  __shared__ double red[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int i = 0; i < n; ++i) {
+    double* ai = a + (long long)i * lda;
+    double acc = 0.0;
+    for (long long l = threadIdx.x; l < m; l += blockDim.x) acc += ai[l] * ai[l];
+    const double norm = sqrt(block_sum(acc, red));
+    if (norm > 0.0)
+      for (long long l = threadIdx.x; l < m; l += blockDim.x) ai[l] /= norm;
+    __syncthreads();
+    for (int j = i + 1 + wid; j < n; j += nw) {
+      double* aj = a + (long long)j * lda;
+      double dot = 0.0;
+      for (long long l = lane; l < m; l += 32) dot += ai[l] * aj[l];
+      dot = warp_sum(dot);
+      for (long long l = lane; l < m; l += 32) aj[l] -= dot * ai[l];
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void orth_defect_kernel(const double* __restrict__ a, long long lda, long long m,
+                                   int n, double* out) {
+  __shared__ double red[32];
+  double worst = 0.0;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int pidx = wid; pidx < n * n; pidx += nw) {
+    const int i = pidx % n, j = pidx / n;
+    if (i > j) continue;
+    double dot = 0.0;
+    for (long long l = lane; l < m; l += 32) dot += a[l + i * lda] * a[l + j * lda];
+    dot = warp_sum(dot);
+    const double d = fabs(dot - (i == j ? 1.0 : 0.0));
+    if (d > worst) worst = d;
+  }
+  // block max
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+  if (lane == 0) red[wid] = worst;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double w = 0.0;
+    for (int i = 0; i < nw; ++i) w = fmax(w, red[i]);
+    *out = w;
+  }
+}
+
+__global__ void unfold_kernel(const double* __restrict__ t, ModeView v, double* __restrict__ a) {
+  const long long total = v.left * v.n * v.right;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    // source-order traversal: idx = l + i left + r left n
+    const long long l = idx % v.left;
+    const long long i = (idx / v.left) % v.n;
+    const long long r = idx / (v.left * v.n);
+    a[i + (l + r * v.left) * v.n] = t[idx];
+  }
+}
+
+__global__ void pad_kernel(const double* __restrict__ t, ModeView v, long long extra,
+                           double* __restrict__ out) {
+  const long long nn = v.n + extra;
+  const long long total = v.left * nn * v.right;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long l = idx % v.left;
+    const long long i = (idx / v.left) % nn;
+    const long long r = idx / (v.left * nn);
+    out[idx] = (i < v.n) ? t[l + i * v.left + r * v.left * v.n] : 0.0;
+  }
+}
+
+__global__ void concat_kernel(const double* __restrict__ a, const double* __restrict__ b,
+                              long long left, long long na, long long nb, long long right,
+                              double* __restrict__ out) {
+  const long long nn = na + nb;
+  const long long total = left * nn * right;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long l = idx % left;
+    const long long i = (idx / left) % nn;
+    const long long r = idx / (left * nn);
+    out[idx] = (i < na) ? a[l + i * left + r * left * na] : b[l + (i - na) * left + r * left * nb];
+  }
+}
+
+__global__ void sumsq_partial_kernel(const double* __restrict__ x, long long n,
+                                     double* __restrict__ partial) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    acc += x[i] * x[i];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = acc;
+}
+
+__global__ void sum_kernel(const double* __restrict__ partial, int n, double* out) {
+  __shared__ double red[32];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) acc += partial[i];
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) *out = acc;
+}
+
+inline int grid_for(long long total, int block = 256, int cap = 148 * 16) {
+  long long g = (total + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace
+
+void launch_sym_eig(const double* g, int n, double* evals, double* evecs, double* work,
+                    int* sweeps_out, cudaStream_t st) {
+  if (n <= 0) return;
+  const size_t smem = sizeof(Rot) * ((n + 2) / 2) + sizeof(int) * (n + 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(sym_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
+  }
+  sym_eig_kernel<<<1, 1024, smem, st>>>(g, n, evals, evecs, work, sweeps_out);
+  ++g_launches;
+}
+
+void launch_truncate(double* evals, int n, double delta, int zero_floor, long long* out_rank,
+                     double* out_disc, cudaStream_t st) {
+  truncate_kernel<<<1, 32, 0, st>>>(evals, n, delta, zero_floor, out_rank, out_disc);
+  ++g_launches;
+}
+
+int gram_splits(int rows, long long cols) {
+  const int nt = (rows + GT - 1) / GT;
+  const int tiles = nt * (nt + 1) / 2;
+  long long s = (2LL * kNumSMs + tiles - 1) / tiles;
+  const long long max_by_cols = (cols + 4 * GK - 1) / (4 * GK);
+  if (s > max_by_cols) s = max_by_cols;
+  if (s > 256) s = 256;
+  if (s < 1) s = 1;
+  return (int)s;
+}
+
+void launch_gram(const double* a, int rows, long long cols, double* g, double* partial,
+                 cudaStream_t st) {
+  const int nt = (rows + GT - 1) / GT;
+  const int tiles = nt * (nt + 1) / 2;
+  const int splits = gram_splits(rows, cols);
+  long long chunk = (cols + splits - 1) / splits;
+  chunk = (chunk + GK - 1) / GK * GK;
+  gram_partial_kernel<<<dim3(tiles, splits), 256, 0, st>>>(a, rows, cols, chunk, partial);
+  gram_reduce_kernel<<<grid_for((long long)rows * rows), 256, 0, st>>>(partial, rows, splits, g);
+  g_launches += 2;
+}
+
+void launch_gram_t(const double* a, long long rows, int cols, double* g, cudaStream_t st) {
+  gram_t_kernel<<<grid_for((long long)cols * cols), 256, 0, st>>>(a, rows, cols, g);
+  ++g_launches;
+}
+
+void launch_gemm_nn(const double* a, long long lda, const double* b, long long ldb, double* c,
+                    long long ldc, long long m, int n, int k, cudaStream_t st) {
+  if (m * n == 0) return;
+  gemm_nn_kernel<<<grid_for(m * n), 256, 0, st>>>(a, lda, b, ldb, c, ldc, m, n, k);
+  ++g_launches;
+}
+
+void launch_scale_cols_invsqrt(double* a, long long lda, long long m, int n, const double* evals,
+                               cudaStream_t st) {
+  if (m * n == 0) return;
+  scale_cols_invsqrt_kernel<<<grid_for(m * n), 256, 0, st>>>(a, lda, m, n, evals);
+  ++g_launches;
+}
+
+void launch_mgs(double* a, long long lda, long long m, int n, cudaStream_t st) {
+  if (n == 0) return;
+  mgs_kernel<<<1, 1024, 0, st>>>(a, lda, m, n);
+  ++g_launches;
+}
+
+void launch_orth_defect(const double* a, long long lda, long long m, int n, double* out,
+                        cudaStream_t st) {
+  orth_defect_kernel<<<1, 1024, 0, st>>>(a, lda, m, n, out);
+  ++g_launches;
+}
+
+void launch_unfold(const double* t, ModeView v, double* a, cudaStream_t st) {
+  unfold_kernel<<<grid_for(v.left * v.n * v.right), 256, 0, st>>>(t, v, a);
+  ++g_launches;
+}
+
+void launch_pad(const double* t, ModeView v, long long extra, double* out, cudaStream_t st) {
+  pad_kernel<<<grid_for(v.left * (v.n + extra) * v.right), 256, 0, st>>>(t, v, extra, out);
+  ++g_launches;
+}
+
+void launch_concat(const double* a, const double* b, long long left, long long na, long long nb,
+                   long long right, double* out, cudaStream_t st) {
+  concat_kernel<<<grid_for(left * (na + nb) * right), 256, 0, st>>>(a, b, left, na, nb, right,
+                                                                    out);
+  ++g_launches;
+}
+
+void launch_sumsq(const double* x, long long n, double* out, double* scratch, cudaStream_t st) {
+  const int g = grid_for(n, 256, 1024);
+  sumsq_partial_kernel<<<g, 256, 0, st>>>(x, n, scratch);
+  sum_kernel<<<1, 1024, 0, st>>>(scratch, g, out);
+  g_launches += 2;
+}
+
+}  // namespace tsg

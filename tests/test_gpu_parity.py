@@ -1,0 +1,165 @@
+"""GPU parity: the B200 path (libtsg.so through its C ABI) against the
+reference's golden fixtures and the pinned CPU oracle, on identical inputs."""
+import numpy as np
+import pytest
+
+import cases
+import parity as P
+
+pytestmark = pytest.mark.gpu
+
+S = pytest.importorskip("paper_2308_16395_b200.streaming")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def run_gpu(case, asynchronous=False):
+    st = S.stream_init(case.init_flat, case.tau, dims=case.init_dims, asynchronous=asynchronous)
+    for s in case.slices:
+        st.stream_update(s)
+    st.synchronize()
+    return st
+
+
+@pytest.mark.parametrize("name", sorted(cases.STREAM_CASES))
+def test_stream_vs_golden(golden, name):
+    case = cases.STREAM_CASES[name]()
+    g = golden("stream_" + name)
+    st = run_gpu(case)
+    sg = st.export()
+    mg = P.metrics_arrays(st.metrics(), sg.order)
+    mc = P.compare_metrics(mg, P.golden_metrics(g), float(g["total_input_sq"]))
+    sc = P.compare_states(sg, P.state_from_golden(g))
+    print(name, mc, sc)
+    P.assert_parity(mc, sc)
+
+
+def test_async_mode_matches_sync(golden):
+    case = cases.case_growth()
+    a = run_gpu(case, asynchronous=True).export()
+    b = run_gpu(case, asynchronous=False).export()
+    assert a.core_dims == b.core_dims
+    np.testing.assert_array_equal(a.core, b.core)
+    np.testing.assert_array_equal(a.left, b.left)
+
+
+def test_blocks_vs_golden(golden):
+    g = golden("blocks")
+    b = cases.blocks_inputs()
+    for name in ("sym", "psd", "diag312"):
+        ev, vec = S.sym_eig_desc(b[name])
+        ref_ev, ref_vec = g[f"eig_{name}_vals"], g[f"eig_{name}_vecs"]
+        scale = np.max(np.abs(ref_ev))
+        assert np.max(np.abs(ev - ref_ev)) <= 1e-13 * scale
+        assert np.max(np.abs(vec - ref_vec)) <= 1e-10
+    for name, thr in (("m", 0.5), ("m", 0.0), ("lowrank", 1e-6)):
+        l, s, r, disc = S.small_svd_truncated(b[name], thr)
+        key = f"ssvd_{name}_{thr:g}"
+        assert len(s) == len(g[key + "_sigma"])
+        assert np.max(np.abs(s - g[key + "_sigma"])) <= 1e-12 * g[key + "_sigma"][0]
+        w = g[key + "_sigma"][None, :] / g[key + "_sigma"][0]
+        assert np.max(np.abs((l - g[key + "_left"]) * w)) <= 1e-10
+        assert np.max(np.abs((r - g[key + "_right"]) * w)) <= 1e-10
+    for name, delta in (("t", 1.0), ("tl", 1e-3)):
+        for mode in range(3):
+            basis, ev, disc = S.mode_subspace(b[name], mode, delta)
+            key = f"msub_{name}_{mode}"
+            ref_b, ref_ev = g[key + "_basis"], g[key + "_evals"]
+            assert basis.shape == ref_b.shape
+            assert np.max(np.abs(ev - ref_ev)) <= 1e-13 * max(ref_ev[0], 1e-300)
+            w = np.sqrt(ref_ev[: ref_b.shape[1]] / ref_ev[0])[None, :]
+            assert np.max(np.abs((basis - ref_b) * w)) <= 1e-9
+    for mode in range(3):
+        a = b["amat"] if mode == 1 else np.ones((2, b["t"].shape[mode]))
+        np.testing.assert_allclose(S.ttm(b["t"], mode, a, False), g[f"ttm_t_{mode}"], rtol=1e-13, atol=1e-13)
+        np.testing.assert_allclose(S.ttm(b["t"], mode, a.T.copy(), True), g[f"ttm_tT_{mode}"], rtol=1e-13, atol=1e-13)
+
+
+def test_error_behaviour():
+    with pytest.raises(S.InvalidArgument):
+        S.stream_init(np.zeros((5, 4, 3)), 0.5)
+    with pytest.raises(S.InvalidArgument):
+        S.stream_init(np.ones(6), 0.5)
+    ok = np.random.default_rng(3).standard_normal((4, 5, 2))
+    for tau in (0.0, 1.0):
+        with pytest.raises(S.InvalidArgument):
+            S.stream_init(ok, tau)
+    with pytest.raises(S.InvalidArgument):
+        S.sym_eig_desc(np.array([[1.0, 2.0], [0.0, 1.0]]))
+
+
+def test_process_mode_out_of_span(oracle):
+    """process_nonstreaming_mode grows the basis (test_streaming.cpp:249-302)."""
+    case = cases.case_edges()
+    x = case.init_flat.reshape(case.init_dims[::-1]).transpose()
+    y = case.slices[2].reshape(case.init_dims[:-1][::-1]).transpose()
+    st = S.stream_init(x, case.tau)
+    ho = oracle.stream_init(x, case.tau)
+    u_before = st.export().factors[0]
+    delta = 1e-6 * np.linalg.norm(y)
+    res, yo = st.process_nonstreaming_mode(y, 0, delta)
+    ro, yr = ho.process_nonstreaming_mode(y, 0, delta)
+    assert res == pytest.approx(ro, rel=1e-12)
+    assert yo.shape == yr.shape
+    u_after = st.export().factors[0]
+    np.testing.assert_array_equal(u_after[:, : u_before.shape[1]], u_before)  # old columns kept
+    assert np.max(np.abs(u_after.T @ u_after - np.eye(u_after.shape[1]))) <= 1e-10
+    np.testing.assert_allclose(yo, yr, rtol=1e-10, atol=1e-12 * np.linalg.norm(y))
+
+
+def test_checkpoint_resume_equals_uninterrupted():
+    """export -> assemble_streaming_state -> continue == uninterrupted
+    (test_io.cpp:209-247, test_cli.cpp:228-269)."""
+    case = cases.case_growth()
+    full = run_gpu(case).export()
+    half = len(case.slices) // 2
+    st = S.stream_init(case.init_flat, case.tau, dims=case.init_dims)
+    for s in case.slices[:half]:
+        st.stream_update(s)
+    snap = st.export()
+    st2 = S.assemble_streaming_state(snap)
+    r = st2.export()
+    np.testing.assert_array_equal(r.core, snap.core)
+    np.testing.assert_array_equal(r.left, snap.left)
+    for s in case.slices[half:]:
+        st2.stream_update(s)
+    out = st2.export()
+    assert out.core_dims == full.core_dims
+    np.testing.assert_array_equal(out.core, full.core)
+    np.testing.assert_array_equal(out.right, full.right)
+
+
+def test_invariants_after_stream():
+    case = cases.case_c3_small()
+    st = run_gpu(case)
+    s = st.export()
+    core = s.core.reshape(-1, s.rank, order="F")
+    np.testing.assert_allclose(core, s.right * s.sigma[None, :], atol=1e-8 * np.linalg.norm(core))
+    for f in s.factors:
+        assert np.max(np.abs(f.T @ f - np.eye(f.shape[1]))) <= 1e-10
+    assert np.max(np.abs(s.right.T @ s.right - np.eye(s.rank))) <= 1e-9
+    assert st.estimate_relative_error() <= case.tau
+
+
+@pytest.mark.slow
+def test_config2_full_size_vs_oracle(oracle):
+    """BASELINE configs[1] (200^3 slices) at full size for the first updates."""
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.CONFIGS["c2"]
+    case = cases.config_case(cfg, n_slices=cfg.n_init + 6)
+    st = run_gpu(case)
+    x = case.init_flat.reshape(case.init_dims[::-1]).transpose()
+    ho = oracle.stream_init(x, case.tau)
+    for s in case.slices:
+        ho.update_flat(s)
+    sg, so = st.export(), ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(st.metrics(), sg.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(sg, so)
+    print("c2", mc, sc)
+    P.assert_parity(mc, sc)
