@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -77,7 +78,7 @@ struct tsg_stream {
   double *left = nullptr, *left2 = nullptr;
   double* slice = nullptr;   // device staging for host slices
   double* slice_b = nullptr; // second caller-visible slice buffer
-  double *w0 = nullptr, *w1 = nullptr;
+  double *w0 = nullptr, *w1 = nullptr, *w2 = nullptr;
   double* ebuf = nullptr;
   double* kbuf = nullptr;
   double* evec = nullptr;
@@ -133,6 +134,13 @@ struct tsg_stream {
   }
 
   void sync() { ck(cudaStreamSynchronize(st), "cudaStreamSynchronize"); }
+  // TSG_DEBUG_SYNC=1: synchronise and check after each orchestration step.
+  bool debug_sync = std::getenv("TSG_DEBUG_SYNC") != nullptr;
+  void dbg(const char* where) {
+    if (!debug_sync) return;
+    ck(cudaStreamSynchronize(st), where);
+    ck(cudaGetLastError(), where);
+  }
 
   void pull_ctrl() {
     ck(cudaMemcpyAsync(ctrl_h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
@@ -336,13 +344,16 @@ struct tsg_stream {
   // Grow U_k by the residual's dominant directions (streaming.cpp:142-151).
   // y: mode input tensor (dims yd); p: its projection; result written to
   // `dst` (concat of p and the carried coefficients), yd updated.
-  void expand_mode(const double* y, long long* yd, int mode, double delta, const double* p,
+  void expand_mode(const double* y, long long* yd, int mode, double delta, double* p,
                    double* dst) {
     if (!ebuf) ebuf = dalloc(slice_elems);
     if (!kbuf) kbuf = dalloc(slice_elems);
     ModeView v{prod(yd, mode), yd[mode], prod(yd + mode + 1, d - 2 - mode)};
-    project(y, yd, mode, nullptr, partial + 2LL * 148 * kMaxD, ebuf);
+    dbg("expand: entry");
+    project(y, yd, mode, p, partial + 2LL * 148 * kMaxD, ebuf);
+    dbg("expand: residual");
     Sub s = mode_subspace(ebuf, yd, d - 1, mode, delta);
+    dbg("expand: mode_subspace");
     const long long g = s.rank;
     if (R[mode] + g > N[mode]) fail(TSG_EOTHER, "expansion exceeds the mode size");
     // carried = W^T E (streaming.cpp:145)
@@ -356,9 +367,19 @@ struct tsg_stream {
     a.partial = nullptr;
     a.residual = 0;
     launch_project(a, st);
+    dbg("expand: carried");
     // U_k <- [U_k W] (old columns untouched)
-    ck(cudaMemcpyAsync(U[mode] + R[mode] * N[mode], s.basis, sizeof(double) * N[mode] * g,
-                       cudaMemcpyDeviceToDevice, st), "hcat");
+    {
+      const cudaError_t e = cudaMemcpyAsync(U[mode] + R[mode] * N[mode], s.basis,
+                                            sizeof(double) * N[mode] * g, cudaMemcpyDeviceToDevice, st);
+      if (e != cudaSuccess) {
+        char buf[256];
+        std::snprintf(buf, sizeof buf, "hcat: %s (mode %d R %lld N %lld g %lld basis %p U %p rows %lld)",
+                      cudaGetErrorString(e), mode, R[mode], N[mode], g, (void*)s.basis,
+                      (void*)U[mode], yd[mode]);
+        fail(TSG_EDEVICE, buf);
+      }
+    }
     // pad core and v (= Q) along mode (tensor.cpp:168-184)
     long long cd[kMaxD];
     for (int k = 0; k + 1 < d; ++k) cd[k] = R[k];
@@ -379,6 +400,7 @@ struct tsg_stream {
     launch_ledger_add_nonstream(ctrl, dd, st);
     // y <- concat_k(P, carried)
     launch_concat(p, kbuf, v.left, R[mode], g, v.right, dst, st);
+    dbg("expand: concat");
     sync();
     dfree(dd);
     dfree(Q); dfree(Q2); dfree(core); dfree(core2);
@@ -397,6 +419,14 @@ struct tsg_stream {
   long long e_alloc_n() const { return evec_n; }
 
   // ---------------------------------------------------------- update
+  // A work buffer that is none of `avoid` (three rotate; slices never
+  // overwrite the caller's input).
+  double* pick(const double* a0, const double* a1) {
+    for (double* b : {w0, w1, w2})
+      if (b != a0 && b != a1) return b;
+    return nullptr;
+  }
+
   void update(const double* y_in, int mem_kind) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
@@ -406,7 +436,9 @@ struct tsg_stream {
          "slice H2D");
       y = slice;
     }
-    // speculative projections of every non-streaming mode
+    // Speculatively project every remaining mode from `base` (the input of
+    // mode m0), decide once, and on a residual above delta rebuild the
+    // expanding mode's input from `base`, grow the basis and continue.
     long long yd[kMaxD];
     for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
     DecideArgs da;
@@ -415,91 +447,71 @@ struct tsg_stream {
     da.nmodes = d - 1;
     da.tau = tau;
     da.order = d;
-    ensure_partial(2LL * 148 * (d - 1) + 16);
-    const double* in[kMaxD];
-    double* outb[kMaxD];
-    const double* cur = y;
-    int off = 0;
-    for (int k = 0; k + 1 < d; ++k) {
-      double* out = (cur == w0) ? w1 : w0;
-      in[k] = cur;
-      outb[k] = out;
-      da.off[k] = off;
-      da.cnt[k] = project(cur, yd, k, out, partial + off);
-      off += 2 * da.cnt[k];
-      yd[k] = R[k];
-      cur = out;
-    }
     da.partial = partial;
-    da.first_mode = 0;
-    launch_decide(da, st);
-    drain_async_pending();
-    pull_ctrl();
-    check_status();
-    r_host = ctrl_h->r;
+    const double* base = y;
+    const double* b = nullptr;
+    int m0 = 0;
     int mask = 0;
-    if (ctrl_h->zero_slice) {
-      launch_commit_modes(ctrl, 0, 0, 1, st);
-      grow_rows(n_d + 1);
-      long long sp[kMaxD] = {0};
-      for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
-      launch_zero_slice(ctrl, left, capr, mdev + mslot, d, sp, st);
-      ++n_d;
-      finish(t0, 0);
-      return;
-    }
-    int em = ctrl_h->expand_mode;
-    if (em < 0) {
-      launch_commit_modes(ctrl, 0, d - 1, 1, st);
-    } else {
-      launch_commit_modes(ctrl, 0, em, 1, st);
-      const double delta = ctrl_h->delta;
-      // dims of the tensor entering mode em
-      long long ydm[kMaxD];
-      for (int k = 0; k + 1 < d; ++k) ydm[k] = (k < em) ? R[k] : N[k];
-      int k = em;
-      const double* yk = in[em];
-      while (true) {
-        // the other work buffer receives the concatenation
-        double* dst = (outb[k] == w0) ? w1 : w0;
-        if (dst == yk && yk != y) {
-          // yk is one of the work buffers and dst aliases it: safe, yk is
-          // no longer needed once E and the carried block are formed.
+    double delta = 0.0;
+    while (true) {
+      long long ydk[kMaxD];
+      std::memcpy(ydk, yd, sizeof yd);
+      const double* cur = base;
+      int off = 0;
+      for (int k = m0; k + 1 < d; ++k) {
+        double* out = pick(cur, base);
+        da.off[k] = off;
+        da.cnt[k] = project(cur, ydk, k, out, partial + off);
+        off += 2 * da.cnt[k];
+        ydk[k] = R[k];
+        cur = out;
+      }
+      da.first_mode = m0;
+      launch_decide(da, st);
+      if (m0 == 0) drain_async_pending();
+      pull_ctrl();
+      check_status();
+      if (m0 == 0) {
+        r_host = ctrl_h->r;
+        delta = ctrl_h->delta;
+        if (ctrl_h->zero_slice) {
+          launch_commit_modes(ctrl, 0, 0, 1, st);
+          grow_rows(n_d + 1);
+          long long sp[kMaxD] = {0};
+          for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
+          launch_zero_slice(ctrl, left, capr, mdev + mslot, d, sp, st);
+          ++n_d;
+          finish(t0, 0);
+          return;
         }
-        if (dst == y) dst = (outb[k] == w0) ? w1 : w0;
-        expand_mode(yk, ydm, k, delta, outb[k], dst);
-        mask |= 1 << k;
-        cur = dst;
-        if (k + 1 >= d - 1) break;
-        // re-project the remaining modes on the grown tensor
-        DecideArgs db = da;
-        int off2 = 0;
-        const double* c2 = dst;
-        for (int kk = k + 1; kk + 1 < d; ++kk) {
-          double* out = (c2 == w0) ? w1 : w0;
-          in[kk] = c2;
-          outb[kk] = out;
-          db.off[kk] = off2;
-          db.cnt[kk] = project(c2, ydm, kk, out, partial + off2);
-          off2 += 2 * db.cnt[kk];
-          ydm[kk] = R[kk];
-          c2 = out;
-        }
-        db.first_mode = k + 1;
-        launch_decide(db, st);
-        pull_ctrl();
-        const int em2 = ctrl_h->expand_mode;
-        cur = c2;
-        if (em2 < 0) {
-          launch_commit_modes(ctrl, k + 1, d - 1, 0, st);
-          break;
-        }
-        launch_commit_modes(ctrl, k + 1, em2, 0, st);
-        for (int kk = em2 + 1; kk + 1 < d; ++kk) ydm[kk] = N[kk];
-        k = em2;
-        yk = in[k];
+      }
+      const int em = ctrl_h->expand_mode;
+      if (em < 0) {
+        launch_commit_modes(ctrl, m0, d - 1, m0 == 0, st);
+        b = cur;
+        break;
+      }
+      launch_commit_modes(ctrl, m0, em, m0 == 0, st);
+      // rebuild the input of mode em (bitwise identical: same kernels, same data)
+      cur = base;
+      for (int k = m0; k < em; ++k) {
+        double* out = pick(cur, base);
+        project(cur, yd, k, out, partial + 2LL * 148 * kMaxD);
+        yd[k] = R[k];
+        cur = out;
+      }
+      double* pbuf = pick(cur, base);
+      double* dst = pick(cur, pbuf);
+      expand_mode(cur, yd, em, delta, pbuf, dst);
+      mask |= 1 << em;
+      base = dst;
+      m0 = em + 1;
+      if (m0 == d - 1) {
+        b = base;
+        break;
       }
     }
+    const double* cur = b;
     // ----- ISVD row insertion + core rotation (isvd.cpp:163-250, streaming.cpp:196-224)
     const int r = ctrl_h->r;
     if (r + 1 > capr) grow_capr(std::max(capr + 16, (r + 1 + 7) / 8 * 8 + 8));
@@ -668,6 +680,7 @@ struct tsg_stream {
     slice_b = dalloc(slice_elems);
     w0 = dalloc(slice_elems);
     w1 = dalloc(slice_elems);
+    w2 = dalloc(slice_elems);
     evec = dalloc(n);
     evec_n = n;
     ensure_isvd_buffers();
@@ -715,7 +728,7 @@ struct tsg_stream {
     free_all();
     for (int k = 0; k < kMaxD; ++k) U[k] = nullptr;
     core = core2 = Q = Q2 = sigma = sigma2 = left = left2 = nullptr;
-    slice = slice_b = w0 = w1 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
+    slice = slice_b = w0 = w1 = w2 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
     partial_cap = ipart_cap = 0;
     evec_n = 0;
     metrics.clear();
@@ -800,7 +813,7 @@ struct tsg_stream {
     pgram = dalloc((long long)capr * capr);
     inner = dalloc(isvd_inner_scratch(capr));
     slice = dalloc(slice_elems); slice_b = dalloc(slice_elems);
-    w0 = dalloc(slice_elems); w1 = dalloc(slice_elems);
+    w0 = dalloc(slice_elems); w1 = dalloc(slice_elems); w2 = dalloc(slice_elems);
     evec = dalloc(n);
     evec_n = n;
     ensure_isvd_buffers();
@@ -900,6 +913,7 @@ int guarded(tsg_stream* h, F&& f) {
     return TSG_OK;
   } catch (const TsgError& e) {
     (h ? h->err : g_free_err) = e.what();
+    cudaGetLastError();  // clear a non-sticky error so later calls start clean
     return e.code;
   } catch (const std::bad_alloc&) {
     (h ? h->err : g_free_err) = "host allocation failed";
