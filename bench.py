@@ -1,0 +1,412 @@
+#!/usr/bin/env python
+"""Benchmark: streamed Tucker slice updates/s (+ GB/s ingested, % roofline).
+
+One step = one ``stream_update`` (reference streaming.cpp:157-233) of one
+synthetic slice of the BASELINE configuration (default configs[1], "c2":
+4-way fp64 200^3 slices, spatial ranks 10, tau 1e-2, init 10 slices).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2]
+    python bench.py --impl reference ...   # the reference's CPU path
+
+Our arm: slices are synthesised on the device before the timed region and
+each step reads a distinct slice (never re-read), so no step hits L2 with
+its input. W untimed updates, then K timed updates bracketed by a barrier and
+synchronisation; time = CUDA events on the engine's stream, max over ranks.
+For N>1 every rank runs an independent replica stream (replicas only; the
+sharded mode of SURVEY §8(e) is not built yet) and value = total slices/s.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "streamed Tucker slice updates/sec"
+UNIT = "slices/s"
+CTRL_BYTES = 200      # sizeof(tsg::Ctrl) read back per synchronisation
+METRICS_BYTES = 184   # sizeof(tsg::Metrics)
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if "Active" in s[2 + i] and "Not" not in s[2 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        backend = "gloo" if args.impl == "reference" else "nccl"
+        if backend == "nccl":
+            import torch
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend=backend)
+    return world, rank, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(world, v: float) -> float:
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def algorithmic_mode0(cfg, ranks):
+    """Mode-0 fused projection kernel: bytes and flops per launch."""
+    n = cfg.slice_elems
+    r0 = ranks[0]
+    nbytes = 8 * (n + n // cfg.slice_dims[0] * r0)   # slice read once + P0 written
+    flops = 4.0 * r0 * n                             # U^T Y and U P (streaming.cpp:129-130)
+    return nbytes, flops
+
+
+def step_algorithmic(cfg, ranks, r, n_d):
+    """Whole-step algorithmic bytes / flops, steady state."""
+    dims = list(cfg.slice_dims)
+    flops, nbytes = 0.0, 8.0 * np.prod(dims)
+    cur = list(dims)
+    for k in range(len(dims)):
+        size = float(np.prod(cur))
+        flops += 4.0 * ranks[k] * size
+        cur[k] = ranks[k]
+        if k >= 1:
+            nbytes += 8.0 * 2 * size
+    n = float(np.prod(ranks[: len(dims)]))
+    flops += 8 * n * r + 2 * n * (r + 1) * r + 2 * n * r * r + 2 * n * r + 2 * n_d * r * r + n_d * r * (r + 1)
+    nbytes += 8.0 * (n * (4 * r + 2 * r) + 2 * n_d * r)
+    return nbytes, flops
+
+
+# ----------------------------------------------------------------- our arm
+def run_ours(args, world, rank, local):
+    import torch
+    from paper_2308_16395_b200 import datagen as dg
+    from paper_2308_16395_b200 import streaming as S
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = dg.CONFIGS[args.config]
+    gen = dg.TuckerStream(cfg)
+    # init batch and step slices synthesised on the device (outside timing)
+    init = torch.cat([gen.slice_torch(t, dev) for t in range(cfg.n_init)])
+    nsl = args.warmup + args.steps
+    slices = [gen.slice_torch(cfg.n_init + i, dev) for i in range(nsl)]
+    torch.cuda.synchronize()
+
+    dmma, dfma = S.measure_fp64_peaks(local)
+    st = S.StreamingState(device=local, asynchronous=True, profile=True)
+    st.init_flat(init, gen.init_dims(), cfg.tau)
+    del init
+    ext = torch.cuda.ExternalStream(st.cuda_stream(), device=dev)
+    for i in range(args.warmup):
+        st.stream_update(slices[i])
+    st.synchronize()
+    st.profile(reset=True)
+    launches0 = st.kernel_launches()
+    clocks = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for i in range(args.warmup, nsl):
+        st.stream_update(slices[i])
+    e1.record(ext)
+    st.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    launches = st.kernel_launches() - launches0
+    prof = st.profile()
+    q = st.query()
+    ms_max = allreduce_max(world, ms)
+    total_slices = allreduce_sum(world, float(args.steps))
+    value = total_slices / (ms_max / 1e3)
+    ranks = q["core_dims"]
+
+    # roofline of the dominant kernel (mode-0 fused projection)
+    hbm, hbm_kind = load_peaks()
+    nbytes, flops = algorithmic_mode0(cfg, ranks)
+    t_mode0 = prof["mode0_ms"] / 1e3
+    t_hbm, t_fp = nbytes / (hbm * 1e9), flops / (dmma * 1e12)
+    if t_hbm >= t_fp:
+        achieved = nbytes / t_mode0 / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm, "peak_source": f"{hbm_kind} MEASURED_PEAKS.json hbm_gbs"}
+    else:
+        achieved = flops / t_mode0 / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": dmma, "unit": "TFLOP/s",
+                "frac": achieved / dmma, "peak_source": "measured FP64 DMMA (tsg_measure_fp64_peaks)"}
+    roof["kernel"] = "project_kernel (mode 0)"
+    roof["algorithmic_bytes_per_launch"] = nbytes
+    roof["algorithmic_flops_per_launch"] = flops
+    roof["avg_launch_ms"] = prof["mode0_ms"]
+    roof["traffic"] = load_traffic(args.config)
+    sb, sf = step_algorithmic(cfg, ranks, q["rank"], q["n_d"])
+    step_s = ms_max / 1e3 / args.steps
+    step_roof = max(sb / (hbm * 1e9), sf / (dmma * 1e12))
+
+    # end to end through the public API with pinned host slices
+    e2e = None
+    if args.e2e_steps > 0:
+        host = [torch.empty(cfg.slice_elems, dtype=torch.float64, pin_memory=True) for _ in range(min(args.e2e_steps, 8))]
+        for j, h in enumerate(host):
+            h.copy_(slices[j % nsl].cpu())
+        st2 = S.StreamingState(device=local, asynchronous=False)
+        st2.init_flat(torch.cat([gen.slice_torch(t, dev) for t in range(cfg.n_init)]), gen.init_dims(), cfg.tau)
+        ext2 = torch.cuda.ExternalStream(st2.cuda_stream(), device=dev)
+        st2.stream_update(host[0])
+        barrier(world)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        f0.record(ext2)
+        for j in range(args.e2e_steps):
+            st2.stream_update(host[j % len(host)])   # H2D inside; sync mode reads the result back
+        f1.record(ext2)
+        st2.synchronize()
+        wall = time.perf_counter() - t0
+        ems = max(f0.elapsed_time(f1), wall * 1e3)
+        ems = allreduce_max(world, ems)
+        e2e = {"value": allreduce_sum(world, float(args.e2e_steps)) / (ems / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": cfg.slice_bytes,
+               "d2h_bytes_per_step": 2 * CTRL_BYTES + METRICS_BYTES,
+               "api": "paper_2308_16395_b200.streaming.StreamingState.stream_update(pinned host)"}
+        st2.close()
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_from_state(args, cfg, st, slices)
+
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "gbs_ingested": value * cfg.slice_bytes / 1e9,
+        "config": {"workload": f"{args.config}: {cfg.notes}", "slice_dims": list(cfg.slice_dims),
+                   "tau": cfg.tau, "eta": cfg.eta, "n_init": cfg.n_init,
+                   "ranks_after": list(ranks), "n_d_after": q["n_d"],
+                   "parallelism": "replicas" if world > 1 else "single",
+                   "l2": "each step reads a distinct device-resident slice (never re-read)",
+                   "mode": "async engine (one decision readback per slice)"},
+        "roofline": roof,
+        "step_roofline_frac": step_roof / step_s,
+        "phases_ms": {k: v for k, v in prof.items() if k != "updates"},
+        "fp64_peak_tflops": {"dmma": dmma, "dfma": dfma},
+        "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+    }
+    st.close()
+    return out
+
+
+def load_traffic(config):
+    p = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    return None
+
+
+def load_reference_lib():
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import py_oracle
+    if py_oracle.reference_available():
+        return py_oracle.load_reference(), "reference"
+    return py_oracle.load_oracle(), "port"
+
+
+def cpu_baseline_from_state(args, cfg, st, slices):
+    """The reference CPU path seeded with our init state through its own
+    assemble_streaming_state, timing a bounded sample of stream_update."""
+    import torch
+    chk, kind = load_reference_lib()
+    state = st_export_for_checker(st)
+    h = chk.assemble(state)
+    n = min(args.cpu_slices, len(slices))
+    host = [slices[i].cpu().numpy() for i in range(n)]
+    t0 = time.perf_counter()
+    for y in host:
+        h.update_flat(y)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{n} stream_update calls of {args.config} slices on the reference "
+                      f"(oracle/_ref, single-threaded) seeded from the GPU init state via "
+                      f"assemble_streaming_state; host {cpu_model()}"}
+
+
+def st_export_for_checker(st):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import py_oracle
+    s = st.export()
+    return py_oracle.State(order=s.order, n_d=s.n_d, rank=s.rank, insertions=s.insertions,
+                           core_dims=s.core_dims, slice_dims=s.slice_dims, tau=s.tau,
+                           squared_error=s.squared_error, total_input_sq=s.total_input_sq,
+                           nonstream_discarded_sq=s.nonstream_discarded_sq, core=s.core,
+                           factors=s.factors, sigma=s.sigma, left=s.left, right=s.right)
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} threads)"
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args, world, rank):
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.CONFIGS[args.config]
+    gen = dg.TuckerStream(cfg)
+    chk, kind = load_reference_lib()
+    x = gen.init_numpy().reshape(gen.init_dims()[::-1]).transpose()
+    t0 = time.perf_counter()
+    h = chk.stream_init(x, cfg.tau)
+    init_s = time.perf_counter() - t0
+    nsl = args.warmup + args.steps
+    slices = [gen.slice_numpy(cfg.n_init + i) for i in range(nsl)]
+    for i in range(args.warmup):
+        h.update_flat(slices[i])
+    t0 = time.perf_counter()
+    for i in range(args.warmup, nsl):
+        h.update_flat(slices[i])
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    sample = (f"{args.steps} timed stream_update calls on {args.config} "
+              f"({'reference sources compiled in place, oracle/_ref' if kind == 'reference' else 'C restatement port'}), "
+              f"single-threaded library; stream_init took {init_s:.1f} s (untimed); host {cpu_model()}")
+    return {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "gbs_ingested": value * cfg.slice_bytes / 1e9,
+        "config": {"workload": f"{args.config}: {cfg.notes}", "slice_dims": list(cfg.slice_dims),
+                   "tau": cfg.tau, "n_init": cfg.n_init, "parallelism": "single"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="c2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--cpu-slices", type=int, default=40)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        # the reference is a single-threaded CPU library: rank 0 alone runs it
+        world = int(os.environ.get("WORLD_SIZE", "1"))
+        rank = int(os.environ.get("RANK", "0"))
+        if rank != 0:
+            return
+        print(json.dumps(run_reference(args, world, rank)))
+        return
+    world, rank, local = dist_setup(args)
+    if False:
+        pass
+    else:
+        out = run_ours(args, world, rank, local)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -60,7 +60,9 @@ enum tsg_mem_kind { TSG_MEM_HOST = 0, TSG_MEM_DEVICE = 1 };
 enum tsg_flags {
   /* tsg_update returns once the work is enqueued; drift and device errors
    * surface at the next call. Default: synchronous, like the reference. */
-  TSG_ASYNC = 1
+  TSG_ASYNC = 1,
+  /* Record CUDA events around the update phases (read with tsg_profile). */
+  TSG_PROFILE = 2
 };
 
 typedef struct tsg_stream tsg_stream;
@@ -129,6 +131,14 @@ void* tsg_cuda_stream(tsg_stream* h);
 /* Device pointer to an internal scratch slice buffer of slice size
  * (for callers that synthesize slices on the device). */
 double* tsg_slice_buffer(tsg_stream* h, int32_t which);
+
+/* Phase timing (TSG_PROFILE): out[0] = updates timed, out[1] = mode-0
+ * projection kernel ms (summed), out[2] = remaining projections + decision
+ * ms, out[3] = ISVD + core rotation ms, out[4] = host gap ms (decision
+ * readback), out[5] = mode-0 kernel launches. n >= 6. Resets when reset != 0. */
+int tsg_profile(tsg_stream* h, double* out, int32_t n, int32_t reset);
+/* FP64 pipe peaks on a device, TFLOP/s: DMMA (mma.sync f64) and DFMA. */
+int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tflops);
 
 /* Device building blocks on host buffers (column-major). */
 int tsg_sym_eig_desc(int64_t n, const double* g, double* evals, double* evecs);

@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -99,6 +100,49 @@ struct tsg_stream {
   double pending_wall = 0.0;
   std::vector<tsg_slice_metrics> metrics;
 
+  // phase profiling (TSG_PROFILE)
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::array<cudaEvent_t, 5>> ev_pending;
+  std::array<cudaEvent_t, 5> ev_cur{};
+  double prof[6] = {0, 0, 0, 0, 0, 0};
+  bool profiling() const { return flags & TSG_PROFILE; }
+  cudaEvent_t ev_get() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      ck(cudaEventCreate(&e), "cudaEventCreate");
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+  void ev_mark(int i) {
+    if (!profiling()) return;
+    ev_cur[i] = ev_get();
+    ck(cudaEventRecord(ev_cur[i], st), "cudaEventRecord");
+  }
+  void ev_commit() {
+    if (!profiling()) return;
+    ev_pending.push_back(ev_cur);
+  }
+  void ev_resolve() {
+    for (auto& t : ev_pending) {
+      float a = 0.f, b = 0.f, c = 0.f, g = 0.f;
+      cudaEventElapsedTime(&a, t[0], t[1]);
+      cudaEventElapsedTime(&b, t[1], t[2]);
+      cudaEventElapsedTime(&g, t[2], t[3]);
+      cudaEventElapsedTime(&c, t[3], t[4]);
+      prof[0] += 1;
+      prof[1] += a;
+      prof[2] += b;
+      prof[3] += c;
+      prof[4] += g;
+      prof[5] += 1;
+      for (auto e : t) ev_pool.push_back(e);
+    }
+    ev_pending.clear();
+  }
+
   long long cur_bytes = 0, peak_bytes = 0;
   std::vector<std::pair<void*, long long>> allocs;
   long long launches_at_create = 0;
@@ -146,6 +190,7 @@ struct tsg_stream {
     ck(cudaMemcpyAsync(ctrl_h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
     sync();
     ck(cudaGetLastError(), "kernel");
+    if (!ev_pending.empty()) ev_resolve();
   }
   void push_ctrl() {
     ck(cudaMemcpyAsync(ctrl, ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl H2D");
@@ -461,13 +506,16 @@ struct tsg_stream {
       for (int k = m0; k + 1 < d; ++k) {
         double* out = pick(cur, base);
         da.off[k] = off;
+        if (k == 0) ev_mark(0);
         da.cnt[k] = project(cur, ydk, k, out, partial + off);
+        if (k == 0) ev_mark(1);
         off += 2 * da.cnt[k];
         ydk[k] = R[k];
         cur = out;
       }
       da.first_mode = m0;
       launch_decide(da, st);
+      if (m0 == 0) ev_mark(2);
       if (m0 == 0) drain_async_pending();
       pull_ctrl();
       check_status();
@@ -544,7 +592,10 @@ struct tsg_stream {
     B.capr = capr;
     B.order = d;
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
+    ev_mark(3);
     launch_isvd(B, st);
+    ev_mark(4);
+    if (mask == 0) ev_commit();
     std::swap(Q, Q2);
     std::swap(core, core2);
     std::swap(sigma, sigma2);
@@ -1087,6 +1138,22 @@ int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out) {
     if (h->metrics.empty()) fail(TSG_EINVAL, "no metrics recorded");
     *out = h->metrics.back();
   });
+}
+
+int tsg_profile(tsg_stream* h, double* out, int32_t n, int32_t reset) {
+  return guarded(h, [&] {
+    h->sync();
+    h->ev_resolve();
+    for (int i = 0; i < n && i < 6; ++i) out[i] = h->prof[i];
+    if (reset)
+      for (double& v : h->prof) v = 0.0;
+  });
+}
+
+int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tflops) {
+  const int st = tsg::measure_fp64_peaks(device, dmma_tflops, dfma_tflops);
+  if (st) g_free_err = "fp64 peak measurement failed";
+  return st;
 }
 
 int64_t tsg_kernel_launches(tsg_stream* h) { return h ? g_launches - h->launches_at_create : g_launches; }

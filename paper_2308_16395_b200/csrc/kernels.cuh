@@ -139,4 +139,6 @@ void launch_coupling_check(Ctrl* ctrl, const double* core, const double* q,
                            const double* sigma, long long n, int r,
                            double* partial, cudaStream_t st);
 
+int measure_fp64_peaks(int device, double* dmma_tflops, double* dfma_tflops);
+
 }  // namespace tsg

@@ -29,7 +29,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtsg.so")
 MAXD = 8
 MEM_HOST, MEM_DEVICE = 0, 1
-ASYNC = 1
+ASYNC, PROFILE = 1, 2
 
 _i64p = C.POINTER(C.c_int64)
 _dp = C.POINTER(C.c_double)
@@ -92,7 +92,8 @@ EXPORTED = [
     "tsg_process_mode", "tsg_query", "tsg_export_state", "tsg_import_state",
     "tsg_estimate_relative_error", "tsg_metrics_count", "tsg_metrics_at", "tsg_last_metrics",
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
-    "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm",
+    "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
+    "tsg_measure_fp64_peaks",
 ]
 
 _LIB = None
@@ -138,6 +139,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                                     _dp, _dp]
     L.tsg_ttm.argtypes = [_dp, C.c_int32, _i64p, C.c_int32, _dp, C.c_int64, C.c_int64, C.c_int32,
                           _dp]
+    L.tsg_profile.argtypes = [C.c_void_p, _dp, C.c_int32, C.c_int32]
+    L.tsg_measure_fp64_peaks.argtypes = [C.c_int32, _dp, _dp]
     _LIB = L
     return L
 
@@ -199,9 +202,10 @@ class StreamingState:
     """Owns one device-resident streaming state (a tsg_stream handle)."""
 
     def __init__(self, device: int = 0, asynchronous: bool = False, rank_capacity: int = 0,
-                 row_capacity: int = 0):
+                 row_capacity: int = 0, profile: bool = False):
         self.L = load_library()
-        cfg = TsgConfig(device, ASYNC if asynchronous else 0, rank_capacity, row_capacity, 0)
+        flags = (ASYNC if asynchronous else 0) | (PROFILE if profile else 0)
+        cfg = TsgConfig(device, flags, rank_capacity, row_capacity, 0)
         h = C.c_void_p()
         code = self.L.tsg_create(C.byref(cfg), C.byref(h))
         if code:
@@ -310,6 +314,13 @@ class StreamingState:
     def estimate_relative_error(self) -> float:
         return float(self.L.tsg_estimate_relative_error(self.h))
 
+    def profile(self, reset: bool = False) -> dict:
+        out = np.zeros(6)
+        self._check(self.L.tsg_profile(self.h, _p(out), 6, int(reset)))
+        n = max(out[0], 1.0)
+        return {"updates": int(out[0]), "mode0_ms": out[1] / n, "rest_proj_ms": out[2] / n,
+                "isvd_ms": out[3] / n, "host_gap_ms": out[4] / n}
+
     def kernel_launches(self) -> int:
         return int(self.L.tsg_kernel_launches(self.h))
 
@@ -383,6 +394,15 @@ def assemble_streaming_state(st: State, device: int = 0, asynchronous: bool = Fa
     out._check(out.L.tsg_import_state(out.h, C.byref(dm), _p(core), _p(fac), _p(sig), _p(left),
                                       _p(right)))
     return out
+
+
+def measure_fp64_peaks(device: int = 0) -> tuple[float, float]:
+    L = load_library()
+    a, b = C.c_double(), C.c_double()
+    code = L.tsg_measure_fp64_peaks(device, C.byref(a), C.byref(b))
+    if code:
+        _raise(code, L.tsg_last_error(None).decode())
+    return a.value, b.value
 
 
 # ------------------------------------------------------------ building blocks
