@@ -383,6 +383,7 @@ struct tsg_stream {
     a.e = e;
     a.partial = part;
     a.residual = 1;
+    a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? 1 : 0;
     return launch_project(a, st);
   }
 

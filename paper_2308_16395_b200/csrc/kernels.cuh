@@ -64,14 +64,15 @@ void launch_concat(const double* a, const double* b, long long left,
 // Fused mode-k projection: P = U^T X_(k), optional residual
 // E = X - U P with per-CTA partials of ||E||^2 and ||X||^2.
 struct ProjArgs {
-  const double* x;
-  ModeView v;
-  const double* u;   // n x R, column-major, ld = v.n
-  int R;
-  double* p;         // (left, R, right) or nullptr
-  double* e;         // (left, n, right) or nullptr
-  double* partial;   // [grid * 2] (res_sq, x_sq) or nullptr
-  int residual;
+  const double* x = nullptr;
+  ModeView v{1, 1, 1};
+  const double* u = nullptr;   // n x R, column-major, ld = v.n
+  int R = 0;
+  double* p = nullptr;         // (left, R, right) or nullptr
+  double* e = nullptr;         // (left, n, right) or nullptr
+  double* partial = nullptr;   // [grid * 2] (res_sq, x_sq) or nullptr
+  int residual = 0;
+  int stream_in = 0;           // input read once: evict-first loads
 };
 // Returns the grid size (number of partial pairs written).
 int launch_project(const ProjArgs& a, cudaStream_t st);

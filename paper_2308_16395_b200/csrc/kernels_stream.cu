@@ -2,7 +2,11 @@
 // proj/src/isvd.cpp): mode-k projection with fused residual norm, the
 // branch decision, ledgers, the incremental SVD row insertion and the core
 // rotation with the coupling check fused into its epilogue.
+#include <cstdio>
+#include <cstdlib>
+
 #include "kernels.cuh"
+#include "proj_dmma.cuh"
 
 namespace tsg {
 
@@ -796,6 +800,22 @@ inline int grid_for(long long total, int block = 256, int cap = 148 * 8) {
 }  // namespace
 
 int launch_project(const ProjArgs& a, cudaStream_t st) {
+  static const bool force_generic = std::getenv("TSG_GENERIC_PROJ") != nullptr;
+  static const bool debug = std::getenv("TSG_DEBUG_SYNC") != nullptr;
+  if (!force_generic) {
+    const int grid = dmma_proj::launch(a, a.stream_in, st);
+    if (debug) {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess)
+        fprintf(stderr, "proj_dmma failed: %s (left %lld N %lld right %lld R %d grid %d)\n",
+                cudaGetErrorString(e), a.v.left, a.v.n, a.v.right, a.R, grid);
+    }
+    if (grid > 0) {
+      ++g_launches;
+      return grid;
+    }
+  }
   const long long N = a.v.n;
   const long long cols = a.v.left * a.v.right;
   const long long budget = 200 * 1024 / 8;  // doubles of shared memory
@@ -808,7 +828,7 @@ int launch_project(const ProjArgs& a, cudaStream_t st) {
   const size_t smem = 8 * ((u_smem ? N * a.R : 0) + N * bc + a.R * bc);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(project_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 205 * 1024);
     attr = true;
   }
   const long long ntiles = (cols + bc - 1) / bc;
