@@ -592,6 +592,7 @@ struct tsg_stream {
     B.n_d = n_d;
     B.capr = capr;
     B.order = d;
+    B.r_hint = r;
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
     ev_mark(3);
     launch_isvd(B, st);
@@ -1156,6 +1157,8 @@ int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tfl
   if (st) g_free_err = "fp64 peak measurement failed";
   return st;
 }
+
+int tsg_debug_isvd_clocks(int64_t* out) { return tsg::read_isvd_clocks(reinterpret_cast<long long*>(out)); }
 
 int64_t tsg_kernel_launches(tsg_stream* h) { return h ? g_launches - h->launches_at_create : g_launches; }
 

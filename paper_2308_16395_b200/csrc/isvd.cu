@@ -1,0 +1,1088 @@
+// Incremental SVD row insertion and streaming-mode core update
+// (reference proj/src/isvd.cpp:163-250 add_row, proj/src/streaming.cpp:196-224
+// core rotation, :39-64 coupling check), entirely on the device.
+//
+// Two execution shapes:
+//  * fused: one CTA performs the whole chain (p_gram, the two projection
+//    passes, the inner SVD, the Q / core / left updates and the coupling
+//    check) when the ISVD width n and rank are small (configs 1, 2, early 5):
+//    one launch per slice, no inter-kernel latency;
+//  * split: grid-wide projection passes and row updates around the same
+//    inner SVD when n is large (configs 3, 4, late 5).
+// The inner SVD of S' = [diag(s) 0; p^T k] follows small_svd_truncated
+// (linalg.cpp:210-259): Gram route S'^T S', Jacobi eigensolve with the
+// reference's stopping rule, stable descending sort, clamp and sign rule,
+// sigma floor, truncation rank, U = S' V / sigma and one MGS pass. The
+// cyclic sweep order is replaced by the round-robin parallel order (every
+// pair once per sweep); for m = r+1 <= 32 it runs in a single warp with no
+// block barriers.
+#include <cstdio>
+
+#include "kernels.cuh"
+#include "secular.cuh"
+
+namespace tsg {
+
+__device__ long long g_isvd_clk[16];
+
+// Scratch layout of the inner SVD (all column-major, in the `inner` buffer).
+struct InnerLayout {
+  long long W, U, M, w, lam, G, V, p, perm, pg;
+  long long total;
+};
+__host__ __device__ inline InnerLayout inner_layout(int capr) {
+  const long long m = capr + 1;
+  InnerLayout L;
+  long long o = 0;
+  L.W = o; o += m * m;     // eigenvectors of S'^T S' (kept columns = right factor Q')
+  L.U = o; o += m * m;     // left factor P' of S'
+  L.M = o; o += m * m;     // core rotation M = P'_top^T p_gram
+  L.w = o; o += m;         // last row of P'
+  L.lam = o; o += m;       // eigenvalues
+  L.G = o; o += m * m;     // global fallback for large inner problems
+  L.V = o; o += m * m;
+  L.p = o; o += m;         // p = p1 + p2
+  L.perm = o; o += m;      // int scratch (stored in doubles' space)
+  L.pg = o; o += m * m;    // p_gram (r x r)
+  L.total = o;
+  return L;
+}
+int isvd_inner_scratch(int capr) { return (int)inner_layout(capr).total; }
+
+int read_isvd_clocks(long long* out) {
+  return cudaMemcpyFromSymbol(out, g_isvd_clk, sizeof(long long) * 16) == cudaSuccess ? 0 : 4;
+}
+
+namespace {
+
+constexpr unsigned FULL = 0xffffffffu;
+#define TSG_CLK(i) \
+  do {             \
+    if (threadIdx.x == 0) g_isvd_clk[i] = clock64(); \
+  } while (0)
+
+struct InnerIO {
+  Ctrl* ctrl;
+  int r;
+  const double* sigma;     // r
+  const double* p;         // r (p1 + p2)
+  double k;                // ||e||
+  int deg;                 // degenerate: residual direction dropped
+  double delta;
+  const double* pgram;     // r x r
+  double* inner;           // scratch (InnerLayout)
+  double* sigma_new;
+  int capr;
+};
+
+__device__ __forceinline__ double Sp(const InnerIO& io, int i, int j) {
+  // S'(i,j): diag(s) stacked over [p^T k] (isvd.cpp:203-209)
+  if (i < io.r) return (i == j) ? io.sigma[j] : 0.0;
+  return (j < io.r) ? io.p[j] : io.k;
+}
+
+// Truncation on the sorted spectrum (linalg.cpp:224-240, isvd.cpp:210-215);
+// single thread. Returns the rank.
+__device__ int inner_truncate(const InnerIO& io, double* lam, int m, int sweeps) {
+  Ctrl* c = io.ctrl;
+  const double smax = sqrt(lam[0]);
+  int rank = 0;
+  double disc = 0.0, margin = 0.0;
+  if (smax > 0.0) {
+    const double fl = kSigmaZeroFactor * smax;
+    for (int i = 0; i < m; ++i)
+      if (sqrt(lam[i]) <= fl) lam[i] = 0.0;
+    const double budget = io.delta * io.delta;
+    double s = 0.0, prev_excess = -1.0;
+    int rr = m;
+    for (int i = m - 1; i >= 0; --i) {
+      const double nx = s + lam[i];
+      if (nx <= budget) {
+        s = nx;
+        rr = i;
+      } else {
+        prev_excess = nx;
+        break;
+      }
+    }
+    rank = rr < 1 ? 1 : rr;
+    for (int j = m - 1; j >= rank; --j) disc += lam[j];
+    if (budget > 0.0) {
+      double mg = fabs(budget - s) / budget;
+      if (prev_excess >= 0.0) mg = fmin(mg, fabs(prev_excess - budget) / budget);
+      margin = mg;
+    }
+  } else {
+    c->status = 3;  // S' == 0 cannot happen with r >= 1 and sigma > 0
+  }
+  c->trunc_margin = margin;
+  c->sweeps = sweeps;
+  double added = disc;
+  if (io.deg) added += io.k * io.k;
+  c->added_error_sq = added;
+  c->squared_error += added;  // isvd.cpp:212-215
+  c->r_new = rank;
+  c->degenerate = io.deg;
+  return rank;
+}
+
+// Whole inner problem in one warp (m = columns of S' <= 32). Shared-memory
+// scratch: G, V, U with pitch 33 (conflict-free), perm (ints).
+__device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sV, double* sU,
+                                 int* perm) {
+  const int lane = threadIdx.x & 31;
+  const int r = io.r;
+  const int m = io.deg ? r : r + 1;
+  const int rows = r + 1;
+  constexpr int P = 33;
+  const InnerLayout L = inner_layout(io.capr);
+  double* lam = io.inner + L.lam;
+  double* W = io.inner + L.W;
+  // S'^T S' = diag(s^2, 0) + z z^T, z = [p; k] (degenerate: diag(s^2) + p p^T)
+  __shared__ double sd[32], sz[32], sQ[32 * 33], sx[8 * 32];
+  __shared__ int si[3 * 32];
+  if (lane < m) {
+    sd[lane] = lane < r ? io.sigma[lane] * io.sigma[lane] : 0.0;
+    sz[lane] = lane < r ? io.p[lane] : io.k;
+  }
+  __syncwarp();
+  TSG_CLK(4);
+  secular::Scratch S;
+  S.sQ = sQ;
+  S.dK = sx;
+  S.wK = sx + 32;
+  S.zK = sx + 64;
+  S.ls = sx + 96;
+  S.lt = sx + 128;
+  S.zh = sx + 160;
+  S.lamall = sx + 192;
+  S.idx = si;
+  S.perm = si + 32;
+  S.flag = si + 64;
+  const int sweep = secular::eig_rank_one(m, sd, sz, S, lam, W, sG);
+  (void)sV;
+  (void)perm;
+  TSG_CLK(5);
+  int rank = 0;
+  if (lane == 0) rank = inner_truncate(io, lam, m, sweep);
+  rank = __shfl_sync(FULL, rank, 0);
+  __syncwarp();
+  TSG_CLK(6);
+  // sigma_new, U = S' W / sigma (multiply, isvd.cpp:217; linalg.cpp:250-256)
+  if (lane < rank) {
+    io.sigma_new[lane] = sqrt(lam[lane]);
+    const double inv = 1.0 / sqrt(lam[lane]);
+    for (int i = 0; i < r; ++i) sU[i * P + lane] = io.sigma[i] * sG[i * P + lane] * inv;
+    double s = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double wl = sG[l * P + lane];
+      if (wl == 0.0) continue;
+      s += sz[l] * wl;
+    }
+    sU[r * P + lane] = s * inv;
+  }
+  __syncwarp();
+  for (int i = 0; i < rank; ++i) {
+    if (lane == i) {
+      double ss = 0.0;
+      for (int l = 0; l < rows; ++l) ss += sU[l * P + i] * sU[l * P + i];
+      const double nrm = sqrt(ss);
+      if (nrm > 0.0)
+        for (int l = 0; l < rows; ++l) sU[l * P + i] /= nrm;
+    }
+    __syncwarp();
+    if (lane > i && lane < rank) {
+      double dot = 0.0;
+      for (int l = 0; l < rows; ++l) dot += sU[l * P + i] * sU[l * P + lane];
+      for (int l = 0; l < rows; ++l) sU[l * P + lane] -= dot * sU[l * P + i];
+    }
+    __syncwarp();
+  }
+  TSG_CLK(7);
+  // outputs: U (P'), M = P'_top^T p_gram, w = last row of P'
+  double* U = io.inner + L.U;
+  double* M = io.inner + L.M;
+  double* w = io.inner + L.w;
+  for (int idx = lane; idx < rows * rank; idx += 32) {
+    const int i = idx % rows, j = idx / rows;
+    U[i + j * rows] = sU[i * P + j];
+  }
+  for (int idx = lane; idx < rank * r; idx += 32) {
+    const int jn = idx % rank, j = idx / rank;
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s += sU[l * P + jn] * io.pgram[l + j * r];
+    M[jn + j * rank] = s;
+  }
+  if (lane < rank) w[lane] = sU[r * P + lane];
+  __syncwarp();
+}
+
+// Block-wide version for m > 32 (G, V in smem when they fit, else global).
+__device__ void inner_solve_block(const InnerIO& io, double* G, double* V) {
+  __shared__ double red[32];
+  __shared__ int sh_rank;
+  struct RotL {
+    double c, s, t;
+    int p, q;
+  };
+  __shared__ RotL rot[128];
+  const InnerLayout L = inner_layout(io.capr);
+  const int r = io.r;
+  const int m = io.deg ? r : r + 1;
+  const int rows = r + 1;
+  double acc = 0.0;
+  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+    const int i = idx % m, j = idx / m;
+    if (i > j) continue;
+    double dot = 0.0;
+    for (int l = 0; l < rows; ++l) dot += Sp(io, l, i) * Sp(io, l, j);
+    G[i + j * m] = dot;
+    G[j + i * m] = dot;
+    acc += (i == j) ? dot * dot : 2.0 * dot * dot;
+  }
+  for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x)
+    V[idx] = ((idx % m) == (idx / m)) ? 1.0 : 0.0;
+  const double tol = kOffDiagTolFactor * sqrt(block_sum(acc, red));
+  const int np = m + (m & 1), half = np / 2;
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    double o2 = 0.0;
+    for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
+      const int i = idx % m, j = idx / m;
+      if (i != j) o2 += G[idx] * G[idx];
+    }
+    const double off = sqrt(block_sum(o2, red));
+    if (off <= tol || m < 2) break;
+    for (int rd = 0; rd < np - 1; ++rd) {
+      for (int mm = threadIdx.x; mm < half; mm += blockDim.x) {
+        int x, y;
+        if (mm == 0) {
+          x = rd % (np - 1);
+          y = np - 1;
+        } else {
+          x = (rd + mm) % (np - 1);
+          y = (rd + np - 1 - mm) % (np - 1);
+        }
+        RotL R;
+        R.p = min(x, y);
+        R.q = max(x, y);
+        R.c = 1.0;
+        R.s = 0.0;
+        R.t = 0.0;
+        if (R.q < m) {
+          const double gpq = G[R.p + R.q * m];
+          if (gpq != 0.0) {
+            const double theta = (G[R.q + R.q * m] - G[R.p + R.p * m]) / (2.0 * gpq);
+            const double t = (theta >= 0.0) ? 1.0 / (theta + sqrt(1.0 + theta * theta))
+                                            : 1.0 / (theta - sqrt(1.0 + theta * theta));
+            const double cc = 1.0 / sqrt(1.0 + t * t);
+            R.c = cc;
+            R.s = t * cc;
+            R.t = t;
+          }
+        }
+        rot[mm] = R;
+      }
+      __syncthreads();
+      for (int bi = threadIdx.x; bi < half * half; bi += blockDim.x) {
+        const int m1 = bi / half, m2 = bi % half;
+        if (m1 > m2) continue;
+        const RotL A = rot[m1], B = rot[m2];
+        const bool idA = (A.s == 0.0 && A.t == 0.0), idB = (B.s == 0.0 && B.t == 0.0);
+        if (idA && idB) continue;
+        const int p1 = A.p, q1 = A.q, p2 = B.p, q2 = B.q;
+        const bool q1v = q1 < m, q2v = q2 < m;
+        if (m1 == m2) {
+          const double gpq = G[p1 + q1 * m], gpp = G[p1 + p1 * m], gqq = G[q1 + q1 * m];
+          G[p1 + p1 * m] = gpp - A.t * gpq;
+          G[q1 + q1 * m] = gqq + A.t * gpq;
+          G[p1 + q1 * m] = 0.0;
+          G[q1 + p1 * m] = 0.0;
+          continue;
+        }
+        const double b00 = G[p1 + p2 * m];
+        const double b01 = q2v ? G[p1 + q2 * m] : 0.0;
+        const double b10 = q1v ? G[q1 + p2 * m] : 0.0;
+        const double b11 = (q1v && q2v) ? G[q1 + q2 * m] : 0.0;
+        const double t00 = A.c * b00 - A.s * b10, t01 = A.c * b01 - A.s * b11;
+        const double t10 = A.s * b00 + A.c * b10, t11 = A.s * b01 + A.c * b11;
+        const double o00 = B.c * t00 - B.s * t01, o01 = B.s * t00 + B.c * t01;
+        const double o10 = B.c * t10 - B.s * t11, o11 = B.s * t10 + B.c * t11;
+        G[p1 + p2 * m] = o00;
+        G[p2 + p1 * m] = o00;
+        if (q2v) {
+          G[p1 + q2 * m] = o01;
+          G[q2 + p1 * m] = o01;
+        }
+        if (q1v) {
+          G[q1 + p2 * m] = o10;
+          G[p2 + q1 * m] = o10;
+        }
+        if (q1v && q2v) {
+          G[q1 + q2 * m] = o11;
+          G[q2 + q1 * m] = o11;
+        }
+      }
+      for (int idx = threadIdx.x; idx < m * half; idx += blockDim.x) {
+        const int i = idx % m, mm = idx / m;
+        const RotL R = rot[mm];
+        if (R.q >= m || (R.s == 0.0 && R.t == 0.0)) continue;
+        const double vp = V[i + R.p * m], vq = V[i + R.q * m];
+        V[i + R.p * m] = R.c * vp - R.s * vq;
+        V[i + R.q * m] = R.s * vp + R.c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  __syncthreads();
+  double* lam = io.inner + L.lam;
+  double* W = io.inner + L.W;
+  int* perm = reinterpret_cast<int*>(io.inner + L.perm);
+  for (int i = threadIdx.x; i < m; i += blockDim.x) {
+    const double di = G[i + i * m];
+    int rk = 0;
+    for (int j = 0; j < m; ++j) {
+      const double dj = G[j + j * m];
+      if (dj > di || (dj == di && j < i)) ++rk;
+    }
+    perm[rk] = i;
+  }
+  __syncthreads();
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = wid; j < m; j += nw) {
+      const int src = perm[j];
+      double lambda = G[src + src * m];
+      if (lambda < 0.0) lambda = 0.0;
+      if (lane == 0) lam[j] = lambda;
+      double best = -1.0;
+      int arg = 0x7fffffff;
+      for (int i = lane; i < m; i += 32) {
+        const double av = fabs(V[i + src * m]);
+        if (av > best) {
+          best = av;
+          arg = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(FULL, best, o);
+        const int oa = __shfl_xor_sync(FULL, arg, o);
+        if (ob > best || (ob == best && oa < arg)) {
+          best = ob;
+          arg = oa;
+        }
+      }
+      const bool flip = V[arg + src * m] < 0.0;
+      for (int i = lane; i < m; i += 32) {
+        const double v = V[i + src * m];
+        W[i + j * m] = flip ? -v : v;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) sh_rank = inner_truncate(io, lam, m, sweep);
+  __syncthreads();
+  const int rank = sh_rank;
+  double* U = io.inner + L.U;
+  for (int j = threadIdx.x; j < rank; j += blockDim.x) io.sigma_new[j] = sqrt(lam[j]);
+  for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) {
+    const int i = idx % rows, j = idx / rows;
+    double s = 0.0;
+    for (int l = 0; l < m; ++l) {
+      const double wl = W[l + j * m];
+      if (wl == 0.0) continue;
+      s += Sp(io, i, l) * wl;
+    }
+    U[i + j * rows] = s * (1.0 / sqrt(lam[j]));
+  }
+  __syncthreads();
+  // MGS, right-looking, thread per column (the reference's sequential dot order)
+  for (int i = 0; i < rank; ++i) {
+    double* ui = U + i * rows;
+    if (threadIdx.x == 0) {
+      double ss = 0.0;
+      for (int l = 0; l < rows; ++l) ss += ui[l] * ui[l];
+      const double nrm = sqrt(ss);
+      if (nrm > 0.0)
+        for (int l = 0; l < rows; ++l) ui[l] /= nrm;
+    }
+    __syncthreads();
+    for (int j = i + 1 + threadIdx.x; j < rank; j += blockDim.x) {
+      double* uj = U + j * rows;
+      double dot = 0.0;
+      for (int l = 0; l < rows; ++l) dot += ui[l] * uj[l];
+      for (int l = 0; l < rows; ++l) uj[l] -= dot * ui[l];
+    }
+    __syncthreads();
+  }
+  double* M = io.inner + L.M;
+  double* w = io.inner + L.w;
+  for (int idx = threadIdx.x; idx < rank * r; idx += blockDim.x) {
+    const int jn = idx % rank, j = idx / rank;
+    double s = 0.0;
+    for (int l = 0; l < r; ++l) s += U[l + jn * rows] * io.pgram[l + j * r];
+    M[jn + j * rank] = s;
+  }
+  for (int j = threadIdx.x; j < rank; j += blockDim.x) w[j] = U[r + j * rows];
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- helpers
+// p_gram = left^T left (isvd.cpp:86-100): per (l, j) sum over rows in
+// order, zero multipliers skipped, mirrored.
+__device__ void pgram_block(const double* __restrict__ left, long long n_d, int capr, int r,
+                            double* pg) {
+  for (int idx = threadIdx.x; idx < r * r; idx += blockDim.x) {
+    const int l = idx % r, j = idx / r;
+    if (l > j) continue;
+    double s = 0.0;
+    for (long long i = 0; i < n_d; ++i) {
+      const double w = left[i * capr + j];
+      if (w == 0.0) continue;
+      s += left[i * capr + l] * w;
+    }
+    pg[l + j * r] = s;
+    pg[j + l * r] = s;
+  }
+}
+
+__device__ void finalize_record(Ctrl* c, double d, double cs, Metrics* rec, int order,
+                                const SpatialRanks& sr) {
+  c->coupling_diff_sq = d;
+  c->core_sq = cs;
+  if (sqrt(d) > kCouplingTol * sqrt(cs) + 1e-300) c->status = 2;  // streaming.cpp:55-63
+  c->r = c->r_new;
+  rec->slice_index = c->n_d;
+  c->n_d += 1;
+  c->insertions += 1;
+  for (int k = 0; k + 1 < order; ++k) rec->ranks[k] = sr.v[k];
+  rec->ranks[order - 1] = c->r;
+  rec->slice_norm = sqrt(c->slice_sq);
+  rec->projected_norm = sqrt(c->proj_sq);
+  for (int k = 0; k + 1 < order; ++k) rec->mode_residuals[k] = sqrt(c->res_sq[k]);
+  const double booked = c->squared_error + c->nonstream_discarded_sq;
+  rec->error_estimate = c->total_input_sq <= 0.0 ? 0.0 : sqrt(fmax(booked, 0.0) / c->total_input_sq);
+  rec->trunc_margin = c->trunc_margin;
+  rec->sweeps = c->sweeps;
+}
+
+// Row update of Q and the core for rows [i0, i1): Qn = [Q q] W,
+// Cn = C M^T + b w^T; returns the coupling partials (isvd.cpp:217-225,
+// streaming.cpp:208-218).
+template <int RMAX>
+__device__ void update_rows(const Ctrl* ctrl, const double* __restrict__ q,
+                            const double* __restrict__ cin, const double* __restrict__ e,
+                            const double* __restrict__ b, const double* W, const double* M,
+                            const double* w, const double* __restrict__ sig_new, long long n,
+                            long long i0, long long i1, long long stride, double* qn, double* cn,
+                            double& dacc, double& cacc) {
+  const int r = ctrl->r, rn = ctrl->r_new, deg = ctrl->degenerate;
+  const int m = deg ? r : r + 1;
+  const double inv = deg ? 0.0 : 1.0 / sqrt(ctrl->e_sq);
+  for (long long i = i0; i < i1; i += stride) {
+    double qr[RMAX + 1], cr[RMAX];
+#pragma unroll
+    for (int l = 0; l < RMAX; ++l) {
+      qr[l] = l < r ? q[i + (long long)l * n] : 0.0;
+      cr[l] = l < r ? cin[i + (long long)l * n] : 0.0;
+    }
+    qr[RMAX] = 0.0;
+    const double qi = deg ? 0.0 : e[i] * inv;
+    const double bi = b[i];
+    for (int jn = 0; jn < rn; ++jn) {
+      double sq = 0.0, sc = 0.0;
+      // zero multipliers are skipped in the reference (matrix.cpp:44-52);
+      // adding 0 * x is exact for finite x, so they are not tested here
+#pragma unroll
+      for (int l = 0; l < RMAX; ++l) {
+        if (l < r) {
+          sq += qr[l] * W[l + jn * m];
+          sc += cr[l] * M[jn + l * rn];
+        }
+      }
+      if (!deg) sq += qi * W[r + jn * m];
+      sc += w[jn] * bi;
+      qn[i + (long long)jn * n] = sq;
+      cn[i + (long long)jn * n] = sc;
+      const double diff = sc - sq * sig_new[jn];
+      dacc += diff * diff;
+      cacc += sc * sc;
+    }
+  }
+}
+
+// Generic (any r) row update reading rows from global memory.
+__device__ void update_rows_generic(const Ctrl* ctrl, const double* __restrict__ q,
+                                    const double* __restrict__ cin, const double* __restrict__ e,
+                                    const double* __restrict__ b, const double* W, const double* M,
+                                    const double* w, const double* __restrict__ sig_new, long long n,
+                                    long long i0, long long i1, long long stride, double* qn,
+                                    double* cn, double& dacc, double& cacc) {
+  const int r = ctrl->r, rn = ctrl->r_new, deg = ctrl->degenerate;
+  const int m = deg ? r : r + 1;
+  const double inv = deg ? 0.0 : 1.0 / sqrt(ctrl->e_sq);
+  for (long long i = i0; i < i1; i += stride) {
+    const double qi = deg ? 0.0 : e[i] * inv;
+    const double bi = b[i];
+    for (int jn = 0; jn < rn; ++jn) {
+      double sq = 0.0, sc = 0.0;
+      for (int l = 0; l < r; ++l) {
+        const double wl = W[l + jn * m];
+        if (wl != 0.0) sq += q[i + (long long)l * n] * wl;
+        const double ml = M[jn + l * rn];
+        if (ml != 0.0) sc += cin[i + (long long)l * n] * ml;
+      }
+      if (!deg) {
+        const double wl = W[r + jn * m];
+        if (wl != 0.0) sq += qi * wl;
+      }
+      const double wj = w[jn];
+      if (wj != 0.0) sc += wj * bi;
+      qn[i + (long long)jn * n] = sq;
+      cn[i + (long long)jn * n] = sc;
+      const double diff = sc - sq * sig_new[jn];
+      dacc += diff * diff;
+      cacc += sc * sc;
+    }
+  }
+}
+
+// left <- blkdiag(left, 1) P' (isvd.cpp:227-237; right_multiply :66-84)
+__device__ void left_rows(const Ctrl* ctrl, const double* __restrict__ left, long long n_d,
+                          int capr, const double* U, double* left_new, long long tid,
+                          long long stride) {
+  const int r = ctrl->r, rn = ctrl->r_new;
+  const int rows = r + 1;
+  const long long total = (n_d + 1) * capr;
+  for (long long idx = tid; idx < total; idx += stride) {
+    const long long i = idx / capr;
+    const int j = (int)(idx % capr);
+    double v = 0.0;
+    if (j < rn) {
+      if (i < n_d) {
+        for (int l = 0; l < r; ++l) v += left[i * capr + l] * U[l + j * rows];
+      } else {
+        v = U[r + j * rows];
+      }
+    }
+    left_new[idx] = v;
+  }
+}
+
+// ============================================================ fused path
+// One CTA (1024 threads); e and the projection coefficients stay on chip.
+template <int RMAX>
+__global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
+  extern __shared__ double fsm[];
+  __shared__ double red[32];
+  __shared__ double sp1[RMAX + 1], sp2[RMAX + 1], sp[RMAX + 1];
+  __shared__ int sperm[33];
+  __shared__ double sh_bsq, sh_esq;
+  Ctrl* c = B.ctrl;
+  const int r = c->r;
+  const long long n = B.n;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const InnerLayout L = inner_layout(B.capr);
+  double* pg = B.inner + L.pg;
+  double* se = fsm;                    // n doubles
+  double* sG = se + n;                 // 32 x 33
+  double* sV = sG + 32 * 33;
+  double* sU = sV + 32 * 33;
+  TSG_CLK(0);
+  // p_gram (old left) and p1 = Q^T b, ||b||^2
+  pgram_block(B.left, B.n_d, B.capr, r, pg);
+  for (int j = wid; j < r; j += 16) {
+    const double* qj = B.q + (long long)j * n;
+    double s = 0.0;
+#pragma unroll 4
+    for (long long i = lane; i < n; i += 32) s += qj[i] * B.b[i];
+    s = warp_sum(s);
+    if (lane == 0) sp1[j] = s;
+  }
+  double bs = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) bs += B.b[i] * B.b[i];
+  bs = block_sum(bs, red);  // includes __syncthreads
+  // e1 = b - Q p1
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < r; ++j) s += B.q[i + (long long)j * n] * sp1[j];
+    se[i] = B.b[i] - s;
+  }
+  __syncthreads();
+  for (int j = wid; j < r; j += 16) {
+    const double* qj = B.q + (long long)j * n;
+    double s = 0.0;
+#pragma unroll 4
+    for (long long i = lane; i < n; i += 32) s += qj[i] * se[i];
+    s = warp_sum(s);
+    if (lane == 0) sp2[j] = s;
+  }
+  __syncthreads();
+  double es = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < r; ++j) s += B.q[i + (long long)j * n] * sp2[j];
+    const double v = se[i] - s;
+    se[i] = v;
+    es += v * v;
+  }
+  es = block_sum(es, red);
+  TSG_CLK(1);
+  for (int j = threadIdx.x; j < r; j += blockDim.x) sp[j] = sp1[j] + sp2[j];
+  if (threadIdx.x == 0) {
+    sh_bsq = bs;
+    sh_esq = es;
+    c->proj_sq = bs;
+    c->e_sq = es;
+  }
+  __syncthreads();
+  // inner SVD in warp 0
+  if (wid == 0) {
+    InnerIO io;
+    io.ctrl = c;
+    io.r = r;
+    io.sigma = B.sigma;
+    io.p = sp;
+    io.k = sqrt(sh_esq);
+    io.deg = (io.k <= kOrthEps * sqrt(sh_bsq)) ? 1 : 0;  // isvd.cpp:191
+    io.delta = c->delta;
+    io.pgram = pg;
+    io.inner = B.inner;
+    io.sigma_new = B.sigma_new;
+    io.capr = B.capr;
+    inner_solve_warp(io, sG, sV, sU, sperm);
+  }
+  __syncthreads();
+  TSG_CLK(2);
+  // stage the small factors, then Q / core rows, coupling partials; left rows
+  double* stW = sU + 32 * 33;
+  double* stM = stW + 33 * 33;
+  double* stw = stM + 33 * 33;
+  double* sts = stw + 33;
+  {
+    const int rr = c->r, rn = c->r_new, mm = c->degenerate ? rr : rr + 1;
+    for (int i = threadIdx.x; i < mm * rn; i += blockDim.x) stW[i] = B.inner[L.W + i];
+    for (int i = threadIdx.x; i < rn * rr; i += blockDim.x) stM[i] = B.inner[L.M + i];
+    for (int i = threadIdx.x; i < rn; i += blockDim.x) {
+      stw[i] = B.inner[L.w + i];
+      sts[i] = B.sigma_new[i];
+    }
+  }
+  __syncthreads();
+  double dacc = 0.0, cacc = 0.0;
+  update_rows<RMAX>(c, B.q, B.c, se, B.b, stW, stM, stw, sts, n, threadIdx.x, n, blockDim.x,
+                    B.qn, B.cn, dacc, cacc);
+  left_rows(c, B.left, B.n_d, B.capr, B.inner + L.U, B.left_new, threadIdx.x, blockDim.x);
+  dacc = block_sum(dacc, red);
+  cacc = block_sum(cacc, red);
+  TSG_CLK(3);
+  if (threadIdx.x == 0) {
+    SpatialRanks sr;
+    for (int k = 0; k < kMaxD; ++k) sr.v[k] = B.spatial_ranks[k];
+    finalize_record(c, dacc, cacc, B.metrics, B.order, sr);
+  }
+}
+
+// ============================================================ split path
+__global__ void pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left, long long n_d,
+                             int capr, double* pg) {
+  pgram_block(left, n_d, capr, ctrl->r, pg);
+}
+
+__global__ void __launch_bounds__(256) isvd_pass1_kernel(const Ctrl* ctrl, const double* __restrict__ q,
+                                                         const double* __restrict__ b, long long n,
+                                                         long long rows_per, int capr,
+                                                         double* __restrict__ part) {
+  const int r = ctrl->r;
+  const long long i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* out = part + (long long)blockIdx.x * (capr + 1);
+  for (int j = wid; j < r; j += nw) {
+    const double* qj = q + (long long)j * n;
+    double s = 0.0;
+#pragma unroll 4
+    for (long long i = i0 + lane; i < i1; i += 32) s += qj[i] * b[i];
+    s = warp_sum(s);
+    if (lane == 0) out[j] = s;
+  }
+  if (wid == nw - 1) {
+    double s = 0.0;
+#pragma unroll 4
+    for (long long i = i0 + lane; i < i1; i += 32) s += b[i] * b[i];
+    s = warp_sum(s);
+    if (lane == 0) out[capr] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) isvd_pass2_kernel(const Ctrl* ctrl, const double* __restrict__ q,
+                                                         const double* __restrict__ b, long long n,
+                                                         long long rows_per, int capr, int nblk,
+                                                         const double* __restrict__ part1,
+                                                         double* __restrict__ e,
+                                                         double* __restrict__ part2) {
+  extern __shared__ double ps[];
+  const int r = ctrl->r;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double s = 0.0;
+    for (int bb = 0; bb < nblk; ++bb) s += part1[(long long)bb * (capr + 1) + j];
+    ps[j] = s;
+  }
+  __syncthreads();
+  const long long i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
+  for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < r; ++j) s += q[i + (long long)j * n] * ps[j];
+    e[i] = b[i] - s;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  double* out = part2 + (long long)blockIdx.x * (capr + 1);
+  for (int j = wid; j < r; j += nw) {
+    const double* qj = q + (long long)j * n;
+    double s = 0.0;
+#pragma unroll 4
+    for (long long i = i0 + lane; i < i1; i += 32) s += qj[i] * e[i];
+    s = warp_sum(s);
+    if (lane == 0) out[j] = s;
+  }
+}
+
+__global__ void __launch_bounds__(256) isvd_pass3_kernel(const Ctrl* ctrl, const double* __restrict__ q,
+                                                         long long n, long long rows_per, int capr,
+                                                         int nblk, const double* __restrict__ part2,
+                                                         double* __restrict__ e,
+                                                         double* __restrict__ part3) {
+  extern __shared__ double ps[];
+  __shared__ double red[32];
+  const int r = ctrl->r;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double s = 0.0;
+    for (int bb = 0; bb < nblk; ++bb) s += part2[(long long)bb * (capr + 1) + j];
+    ps[j] = s;
+  }
+  __syncthreads();
+  const long long i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
+  double acc = 0.0;
+  for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
+    double s = 0.0;
+#pragma unroll 4
+    for (int j = 0; j < r; ++j) s += q[i + (long long)j * n] * ps[j];
+    const double v = e[i] - s;
+    e[i] = v;
+    acc += v * v;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) part3[blockIdx.x] = acc;
+}
+
+struct InnerArgs {
+  Ctrl* ctrl;
+  const double* sigma;
+  double* sigma_new;
+  const double* part1;
+  const double* part2;
+  const double* part3;
+  int nblk;
+  int capr;
+  double* inner;
+  int use_smem;
+};
+
+__global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
+  extern __shared__ double ism[];
+  __shared__ double red[32];
+  __shared__ double sh_bsq, sh_esq;
+  __shared__ int sperm[33];
+  const InnerLayout L = inner_layout(a.capr);
+  Ctrl* c = a.ctrl;
+  const int r = c->r;
+  double* p = a.inner + L.p;
+  for (int j = threadIdx.x; j < r; j += blockDim.x) {
+    double s1 = 0.0, s2 = 0.0;
+    for (int b = 0; b < a.nblk; ++b) s1 += a.part1[(long long)b * (a.capr + 1) + j];
+    for (int b = 0; b < a.nblk; ++b) s2 += a.part2[(long long)b * (a.capr + 1) + j];
+    p[j] = s1 + s2;
+  }
+  double bs = 0.0, es = 0.0;
+  for (int b = threadIdx.x; b < a.nblk; b += blockDim.x) {
+    bs += a.part1[(long long)b * (a.capr + 1) + a.capr];
+    es += a.part3[b];
+  }
+  bs = block_sum(bs, red);
+  es = block_sum(es, red);
+  if (threadIdx.x == 0) {
+    sh_bsq = bs;
+    sh_esq = es;
+    c->proj_sq = bs;
+    c->e_sq = es;
+  }
+  __syncthreads();
+  InnerIO io;
+  io.ctrl = c;
+  io.r = r;
+  io.sigma = a.sigma;
+  io.p = p;
+  io.k = sqrt(sh_esq);
+  io.deg = (io.k <= kOrthEps * sqrt(sh_bsq)) ? 1 : 0;
+  io.delta = c->delta;
+  io.pgram = a.inner + L.pg;
+  io.inner = a.inner;
+  io.sigma_new = a.sigma_new;
+  io.capr = a.capr;
+  const int m = io.deg ? r : r + 1;
+  if (m <= 32) {
+    if (threadIdx.x < 32) {
+      double* sG = ism;
+      inner_solve_warp(io, sG, sG + 32 * 33, sG + 64 * 33, sperm);
+    }
+  } else {
+    double* G = a.use_smem ? ism : a.inner + L.G;
+    double* V = a.use_smem ? ism + (long long)m * m : a.inner + L.V;
+    inner_solve_block(io, G, V);
+  }
+}
+
+template <int RMAX>
+__global__ void __launch_bounds__(256) isvd_update_kernel(const Ctrl* ctrl, const double* __restrict__ q,
+                                                          const double* __restrict__ cin,
+                                                          const double* __restrict__ e,
+                                                          const double* __restrict__ b,
+                                                          const double* __restrict__ inner,
+                                                          const double* __restrict__ sigma_new,
+                                                          long long n, int capr,
+                                                          double* __restrict__ qn,
+                                                          double* __restrict__ cn,
+                                                          double* __restrict__ part) {
+  __shared__ double red[32];
+  const InnerLayout L = inner_layout(capr);
+  double dacc = 0.0, cacc = 0.0;
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  if constexpr (RMAX > 0)
+    update_rows<RMAX>(ctrl, q, cin, e, b, inner + L.W, inner + L.M, inner + L.w, sigma_new, n, tid,
+                      n, stride, qn, cn, dacc, cacc);
+  else
+    update_rows_generic(ctrl, q, cin, e, b, inner + L.W, inner + L.M, inner + L.w, sigma_new, n,
+                        tid, n, stride, qn, cn, dacc, cacc);
+  dacc = block_sum(dacc, red);
+  cacc = block_sum(cacc, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = dacc;
+    part[2 * blockIdx.x + 1] = cacc;
+  }
+}
+
+__global__ void isvd_left_kernel(const Ctrl* ctrl, const double* __restrict__ left, long long n_d,
+                                 int capr, const double* __restrict__ inner,
+                                 double* __restrict__ left_new) {
+  const InnerLayout L = inner_layout(capr);
+  left_rows(ctrl, left, n_d, capr, inner + L.U, left_new,
+            blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
+}
+
+__global__ void isvd_finalize_kernel(Ctrl* c, const double* __restrict__ part, int nblk,
+                                     Metrics* rec, int order, SpatialRanks sr) {
+  __shared__ double red[32];
+  double d = 0.0, cs = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+    d += part[2 * b];
+    cs += part[2 * b + 1];
+  }
+  d = block_sum(d, red);
+  cs = block_sum(cs, red);
+  if (threadIdx.x == 0) finalize_record(c, d, cs, rec, order, sr);
+}
+
+// ------------------------------------------------------- other entry points
+__global__ void zero_slice_kernel(Ctrl* c, double* left, int capr, Metrics* rec, int order,
+                                  SpatialRanks sr) {
+  const long long nd = c->n_d;
+  for (int j = threadIdx.x; j < capr; j += blockDim.x) left[nd * capr + j] = 0.0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  rec->slice_index = nd;
+  c->n_d = nd + 1;
+  for (int k = 0; k + 1 < order; ++k) rec->ranks[k] = sr.v[k];
+  rec->ranks[order - 1] = c->r;
+  rec->slice_norm = 0.0;
+  rec->projected_norm = 0.0;
+  for (int k = 0; k + 1 < order; ++k) rec->mode_residuals[k] = 0.0;
+  const double booked = c->squared_error + c->nonstream_discarded_sq;
+  rec->error_estimate = c->total_input_sq <= 0.0 ? 0.0 : sqrt(fmax(booked, 0.0) / c->total_input_sq);
+  rec->trunc_margin = 0.0;
+  rec->sweeps = 0;
+}
+
+__global__ void init_isvd_kernel(Ctrl* c, const double* __restrict__ core, long long n, int r,
+                                 const double* __restrict__ lam, double* __restrict__ q,
+                                 double* __restrict__ sigma, const double* __restrict__ left_cm,
+                                 long long n_init, double* __restrict__ left_rm, int capr) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long idx = tid; idx < n * r; idx += stride) {
+    const int j = (int)(idx / n);
+    const double inv = 1.0 / sqrt(lam[j]);  // streaming.cpp:96-108
+    q[idx] = core[idx] * inv;
+  }
+  for (long long idx = tid; idx < n_init * capr; idx += stride) {
+    const long long i = idx / capr;
+    const int j = (int)(idx % capr);
+    left_rm[idx] = j < r ? left_cm[i + j * n_init] : 0.0;
+  }
+  if (tid < r) sigma[tid] = sqrt(lam[tid]);
+  if (tid == 0) {
+    c->r = r;
+    c->n_d = n_init;
+    c->insertions = 0;
+  }
+}
+
+__global__ void coupling_kernel(Ctrl* c, const double* __restrict__ core,
+                                const double* __restrict__ q, const double* __restrict__ sigma,
+                                long long n, int r) {
+  __shared__ double red[32];
+  double d = 0.0, cs = 0.0;
+  for (long long idx = threadIdx.x; idx < n * r; idx += blockDim.x) {
+    const int j = (int)(idx / n);
+    const double cv = core[idx];
+    const double diff = cv - q[idx] * sigma[j];
+    d += diff * diff;
+    cs += cv * cv;
+  }
+  d = block_sum(d, red);
+  cs = block_sum(cs, red);
+  if (threadIdx.x == 0) {
+    c->coupling_diff_sq = d;
+    c->core_sq = cs;
+    c->status = (sqrt(d) > kCouplingTol * sqrt(cs) + 1e-300) ? 2 : 0;
+  }
+}
+
+inline int grid_for(long long total, int block = 256, int cap = 148 * 8) {
+  long long g = (total + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+// Dynamic shared memory beyond the default needs the attribute whenever
+// static + dynamic exceeds 48 KB; set it for every requested size.
+template <class K>
+void ensure_smem(K kernel, size_t bytes) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+}  // namespace
+
+// Fused single-CTA chain when n <= kFusedRows and r + 1 <= 32.
+constexpr long long kFusedRows = 12288;
+
+void launch_isvd(const IsvdBufs& B, cudaStream_t st) {
+  const long long n = B.n;
+  const int capr = B.capr;
+  SpatialRanks sr;
+  for (int k = 0; k < kMaxD; ++k) sr.v[k] = B.spatial_ranks[k];
+  if (n <= kFusedRows && B.r_hint + 1 <= 32 && B.r_hint >= 1) {
+    const size_t smem = sizeof(double) * (n + 3 * 32 * 33 + 2 * 33 * 33 + 66);
+    switch ((B.r_hint + 3) / 4) {
+#define TSG_FUSED(R)                                  \
+  case R / 4:                                         \
+    ensure_smem(isvd_fused_kernel<R>, smem);          \
+    isvd_fused_kernel<R><<<1, 512, smem, st>>>(B);    \
+    break;
+      TSG_FUSED(4)
+      TSG_FUSED(8)
+      TSG_FUSED(12)
+      TSG_FUSED(16)
+      TSG_FUSED(20)
+      TSG_FUSED(24)
+      TSG_FUSED(28)
+      TSG_FUSED(32)
+#undef TSG_FUSED
+    }
+    g_launches += 1;
+    return;
+  }
+  long long rows_per = 256;
+  long long nblk = (n + rows_per - 1) / rows_per;
+  if (nblk > 296) {
+    nblk = 296;
+    rows_per = (n + nblk - 1) / nblk;
+  }
+  const int nb = (int)nblk;
+  double* part1 = B.partial;
+  double* part2 = part1 + (long long)nb * (capr + 1);
+  double* part3 = part2 + (long long)nb * (capr + 1);
+  double* part4 = part3 + nb;
+  const InnerLayout L = inner_layout(capr);
+  pgram_kernel<<<1, 256, 0, st>>>(B.ctrl, B.left, B.n_d, capr, B.inner + L.pg);
+  isvd_pass1_kernel<<<nb, 256, 0, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr, part1);
+  isvd_pass2_kernel<<<nb, 256, sizeof(double) * capr, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr,
+                                                            nb, part1, B.e, part2);
+  isvd_pass3_kernel<<<nb, 256, sizeof(double) * capr, st>>>(B.ctrl, B.q, n, rows_per, capr, nb,
+                                                            part2, B.e, part3);
+  InnerArgs ia;
+  ia.ctrl = B.ctrl;
+  ia.sigma = B.sigma;
+  ia.sigma_new = B.sigma_new;
+  ia.part1 = part1;
+  ia.part2 = part2;
+  ia.part3 = part3;
+  ia.nblk = nb;
+  ia.capr = capr;
+  ia.inner = B.inner;
+  const long long m = capr + 1;
+  size_t smem = 2 * m * m * sizeof(double);
+  ia.use_smem = smem <= 160 * 1024 ? 1 : 0;
+  if (!ia.use_smem) smem = 0;
+  smem = std::max(smem, sizeof(double) * 3 * 32 * 33);
+  ensure_smem(isvd_inner_kernel, smem);
+  isvd_inner_kernel<<<1, 512, smem, st>>>(ia);
+  const int gu = grid_for(n, 256, 148 * 4);
+  if (capr <= 16)
+    isvd_update_kernel<16><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
+                                               capr, B.qn, B.cn, part4);
+  else if (capr <= 32)
+    isvd_update_kernel<32><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
+                                               capr, B.qn, B.cn, part4);
+  else if (capr <= 48)
+    isvd_update_kernel<48><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
+                                               capr, B.qn, B.cn, part4);
+  else
+    isvd_update_kernel<0><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
+                                              capr, B.qn, B.cn, part4);
+  isvd_left_kernel<<<grid_for((B.n_d + 1) * capr), 256, 0, st>>>(B.ctrl, B.left, B.n_d, capr,
+                                                                  B.inner, B.left_new);
+  isvd_finalize_kernel<<<1, 256, 0, st>>>(B.ctrl, part4, gu, B.metrics, B.order, sr);
+  g_launches += 8;
+}
+
+void launch_zero_slice(Ctrl* ctrl, double* left, int capr, Metrics* rec, int order,
+                       const long long* spatial, cudaStream_t st) {
+  SpatialRanks sr;
+  for (int k = 0; k < kMaxD; ++k) sr.v[k] = spatial[k];
+  zero_slice_kernel<<<1, 256, 0, st>>>(ctrl, left, capr, rec, order, sr);
+  ++g_launches;
+}
+
+void launch_init_isvd(Ctrl* ctrl, const double* core, long long n, int r, const double* evals_last,
+                      double* q, double* sigma, const double* left_cm, long long n_init,
+                      double* left_rm, int capr, cudaStream_t st) {
+  const long long total = n * r > n_init * capr ? n * r : n_init * capr;
+  init_isvd_kernel<<<grid_for(total), 256, 0, st>>>(ctrl, core, n, r, evals_last, q, sigma,
+                                                    left_cm, n_init, left_rm, capr);
+  ++g_launches;
+}
+
+void launch_coupling_check(Ctrl* ctrl, const double* core, const double* q, const double* sigma,
+                           long long n, int r, double* partial, cudaStream_t st) {
+  (void)partial;
+  coupling_kernel<<<1, 1024, 0, st>>>(ctrl, core, q, sigma, n, r);
+  ++g_launches;
+}
+
+}  // namespace tsg

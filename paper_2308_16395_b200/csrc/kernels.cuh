@@ -122,10 +122,12 @@ struct IsvdBufs {
   long long n_d;       // rows of left before the insertion
   int capr;
   int order;
+  int r_hint;          // streaming rank before the insertion (host mirror)
   long long spatial_ranks[kMaxD];
 };
 void launch_isvd(const IsvdBufs& b, cudaStream_t st);
 int isvd_inner_scratch(int capr);
+int read_isvd_clocks(long long* out);
 
 // Zero slice (streaming.cpp:171-185).
 void launch_zero_slice(Ctrl* ctrl, double* left, int capr, Metrics* rec,

@@ -29,7 +29,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 template <int RT, int MC>
 constexpr int red_doubles() {
-  return 8 * MC * RT * 2 * 32;
+  return 9 * MC * RT * 2 * 32;  // 8 warp partials + the reduced copy
 }
 
 template <int RT, int MC, int GM>
@@ -44,9 +44,15 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
   const int ngroups = (int)((N + 7) / 8);
   double* Us = sm;
   double* red = Us + (long long)ngroups * 8 * RPAD;
-  for (int idx = threadIdx.x; idx < ngroups * 8 * RPAD; idx += blockDim.x) {
-    const int row = idx / RPAD, col = idx % RPAD;
-    Us[idx] = (row < N && col < R) ? a.u[row + (long long)col * N] : 0.0;
+  {
+    // coalesced read of the column-major U, transposed into the padded rows
+    const int rows8 = ngroups * 8;
+    const int total = rows8 * RPAD;
+#pragma unroll 4
+    for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
+      const int col = idx / rows8, row = idx - col * rows8;
+      Us[row * RPAD + col] = (row < N && col < R) ? __ldg(a.u + row + (long long)col * N) : 0.0;
+    }
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -55,13 +61,20 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
   const double* __restrict__ x = a.x;
 
   double X[MC][GM][2], Xn[MC][GM][2];
+  // column c = l + r*left starts at r*left*N + l = c*N - l*(N-1); 32-bit
+  // division only (cols < 2^31 is checked at launch), none when left == 1
+  const unsigned uleft = (unsigned)left;
+  auto col_base = [&](long long c) -> long long {
+    if (uleft == 1u) return c * N;
+    const unsigned l = (unsigned)c % uleft;
+    return c * N - (long long)l * (N - 1);
+  };
   auto load_tile = [&](long long tile, double (&dst)[MC][GM][2]) {
 #pragma unroll
     for (int mc = 0; mc < MC; ++mc) {
       const long long c = tile * 8 * MC + 8 * mc + g;
       const bool cv = c < cols;
-      const long long l = cv ? c % left : 0, r = cv ? c / left : 0;
-      const long long base = r * left * N + l;
+      const long long base = cv ? col_base(c) : 0;
 #pragma unroll
       for (int gi = 0; gi < GM; ++gi) {
         const int grp = warp + 8 * gi;
@@ -88,6 +101,7 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
   double racc = 0.0, xacc = 0.0;
   long long tile = blockIdx.x;
   if (tile < ntiles) load_tile(tile, X);
+#pragma unroll 1
   for (; tile < ntiles; tile += gridDim.x) {
     const long long next = tile + gridDim.x;
     if (next < ntiles) load_tile(next, Xn);
@@ -114,7 +128,7 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
         }
       }
     }
-    // ---- cross-warp reduction (fixed order: deterministic)
+    // ---- cross-warp reduction (reduce-scatter then gather; fixed order)
     double* myred = red + warp * (PER * 32);
 #pragma unroll
     for (int mc = 0; mc < MC; ++mc)
@@ -123,26 +137,29 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
 #pragma unroll
         for (int i = 0; i < 2; ++i) myred[((mc * RT + rt) * 2 + i) * 32 + lane] = acc[mc][rt][i];
     __syncthreads();
+    double* fin = red + 8 * (PER * 32);
+    for (int slot = warp; slot < PER; slot += 8) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sacc += red[w * (PER * 32) + slot * 32 + lane];
+      fin[slot * 32 + lane] = sacc;
+    }
+    __syncthreads();
 #pragma unroll
     for (int mc = 0; mc < MC; ++mc)
 #pragma unroll
       for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          double s = 0.0;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) s += red[w * (PER * 32) + ((mc * RT + rt) * 2 + i) * 32 + lane];
-          acc[mc][rt][i] = s;
-        }
-    __syncthreads();
+        for (int i = 0; i < 2; ++i) acc[mc][rt][i] = fin[((mc * RT + rt) * 2 + i) * 32 + lane];
     // ---- store P (each (mc, rt) block written by one warp)
     if (a.p) {
 #pragma unroll
       for (int mc = 0; mc < MC; ++mc) {
         const long long c = tile * 8 * MC + 8 * mc + g;
         if (c < cols) {
-          const long long l = c % left, r = c / left;
-          double* pout = a.p + r * left * R + l;
+          // (l, r) -> r*left*R + l = c*R - l*(R-1)
+          const long long l = (uleft == 1u) ? 0 : (long long)((unsigned)c % uleft);
+          double* pout = a.p + c * R - l * (R - 1);
 #pragma unroll
           for (int rt = 0; rt < RT; ++rt) {
             if (((mc * RT + rt) & 7) != warp) continue;
@@ -187,11 +204,11 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
             for (int mc = 0; mc < MC; ++mc) {
               const long long c = tile * 8 * MC + 8 * mc + g;
               if (c < cols) {
-                const long long l = c % left, r = c / left;
+                const long long cb = col_base(c);
 #pragma unroll
                 for (int i = 0; i < 2; ++i) {
                   const long long row = 8LL * grp + 2 * t + i;
-                  if (row < N) a.e[r * left * N + row * left + l] = X[mc][gi][i] - c2[mc][i];
+                  if (row < N) a.e[cb + row * left] = X[mc][gi][i] - c2[mc][i];
                 }
               }
             }
@@ -267,9 +284,10 @@ inline int dispatch_rt(const ProjArgs& a, int streaming_in, cudaStream_t st) {
 inline int launch(const ProjArgs& a, int streaming_in, cudaStream_t st) {
   const long long N = a.v.n;
   if (N > 512 || a.R > 64 || a.R < 1) return -1;
+  if (a.v.left * a.v.right >= (1LL << 31) || a.v.left >= (1LL << 31)) return -1;
   const int RT = (a.R + 7) / 8;
   const long long ngroups = (N + 7) / 8;
-  const long long smem = 8 * (ngroups * 8 * (8 * RT + 4)) + 8LL * 8 * 2 * RT * 2 * 32 * 2;
+  const long long smem = 8 * (ngroups * 8 * (8 * RT + 4)) + 8LL * 9 * 4 * RT * 2 * 32;
   if (smem > 220 * 1024) return -1;
   const int GM = (int)((ngroups + 7) / 8);
   if (GM <= 1) return dispatch_rt<1>(a, streaming_in, st);

@@ -1,0 +1,302 @@
+// Eigendecomposition of D + z z^T in one warp (secular equation), for the
+// ISVD inner problem: S'^T S' = diag(s_1^2, ..., s_r^2, 0) + z z^T with
+// z = [p; k] (isvd.cpp:201-209). The reference obtains the same spectrum by
+// cyclic Jacobi on the explicitly formed Gram matrix (linalg.cpp:120-181);
+// here each lane solves one root of f(l) = 1 + sum_i z_i^2 / (d_i - l) with a
+// bracketed one-pole rational iteration, eigenvectors come from Loewner's
+// formula (numerically orthogonal), and tiny z_i / close poles are deflated.
+// Output: eigenvalues descending (clamped >= 0) and eigenvectors with the
+// reference's sign rule, ready for the truncation rule.
+#pragma once
+#include <cfloat>
+
+namespace tsg {
+namespace secular {
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int P = 33;  // shared-memory pitch
+
+// 1/x to full double precision: hardware approximation + two Newton steps.
+__device__ __forceinline__ double rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+
+// f(tau) pieces around origin pole o: returns f, accumulates phi' (without o)
+// and erretm (sum of |terms|).
+__device__ __forceinline__ void eval(const double* dK, const double* wK, int K, int o,
+                                     double sigma, double tau, double& f, double& phi_out,
+                                     double& dphi, double& err) {
+  double phi = 0.0, dp = 0.0, ea = 0.0;
+  for (int i = 0; i < K; ++i) {
+    if (i == o) continue;
+    const double ri = rcp((dK[i] - sigma) - tau);
+    const double q = wK[i] * ri;
+    phi += q;
+    dp += q * ri;
+    ea += fabs(q);
+  }
+  const double qo = -wK[o] * rcp(tau);
+  f = 1.0 + phi + qo;
+  phi_out = phi;
+  dphi = dp;
+  err = 1.0 + ea + fabs(qo);
+}
+
+// Solve root j (0 = largest) of the non-deflated problem (poles dK
+// descending, weights wK = z^2 > 0). Returns origin index and offset tau.
+__device__ int solve_root(const double* dK, const double* wK, int K, double wsum, int j,
+                          int& o_out, double& tau_out) {
+  int o;
+  double lo, hi;  // bracket in tau: f(lo) < 0 < f(hi)
+  if (j == 0) {
+    o = 0;
+    lo = 0.0;
+    hi = wsum;
+  } else {
+    const double mid = 0.5 * (dK[j] + dK[j - 1]);
+    // f at the midpoint, origin-free
+    double fm = 1.0;
+    for (int i = 0; i < K; ++i) fm += wK[i] * rcp(dK[i] - mid);
+    if (fm >= 0.0) {  // root in (d_j, mid]: origin = lower pole d_j
+      o = j;
+      lo = 0.0;
+      hi = mid - dK[j];
+    } else {          // root in (mid, d_{j-1}): origin = upper pole
+      o = j - 1;
+      lo = mid - dK[j - 1];
+      hi = 0.0;
+    }
+  }
+  const double sigma = dK[o];
+  const bool pos = (o == j);  // tau > 0 when the origin is the lower pole
+  double tau = 0.5 * (lo + hi);
+  if (tau == 0.0) tau = pos ? hi : lo;
+  int it = 0;
+  for (; it < 60; ++it) {
+    double f, phi, dphi, err;
+    eval(dK, wK, K, o, sigma, tau, f, phi, dphi, err);
+    if (f < 0.0)
+      lo = tau;
+    else
+      hi = tau;
+    if (fabs(f) <= 8.0 * DBL_EPSILON * err) break;
+    // one-pole + linear model: 1 + phi + phi'(t - tau) - w_o / t = 0
+    const double A = 1.0 + phi - dphi * tau;
+    const double Dd = A * A + 4.0 * dphi * wK[o];
+    const double sq = sqrt(Dd);
+    double t;
+    if (dphi > 0.0) {
+      if (pos)
+        t = (A > 0.0) ? 2.0 * wK[o] / (A + sq) : (-A + sq) / (2.0 * dphi);
+      else
+        t = (A < 0.0) ? 2.0 * wK[o] / (A - sq) : (-A - sq) / (2.0 * dphi);
+    } else {
+      t = wK[o] / A;  // single pole: (1 + phi) t = w_o
+    }
+    if (!(t > lo && t < hi)) t = 0.5 * (lo + hi);
+    if (fabs(t - tau) <= 2.0 * DBL_EPSILON * fabs(tau)) {
+      tau = t;
+      break;
+    }
+    tau = t;
+    if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) break;
+  }
+  o_out = o;
+  tau_out = tau;
+  return it;
+}
+
+// Full solve in warp 0. d (m, descending, >= 0) and z (m) in shared memory.
+// Outputs lam (m, descending) and W (m x m column-major, ld m), plus the
+// same sorted eigenvectors in sW (pitch P) for the caller.
+// Scratch (shared): sQ (m x P, rotations), dK, wK, sig, tau (each 32),
+// idx, perm (int 32), defl flags.
+struct Scratch {
+  double* sQ;      // 32 x P
+  double* dK;      // 32
+  double* wK;      // 32
+  double* zK;      // 32
+  double* ls;      // 32 (sigma of root)
+  double* lt;      // 32 (tau of root)
+  double* zh;      // 32 (Loewner z-hat)
+  double* lamall;  // 32
+  int* idx;        // 32 non-deflated coordinates
+  int* perm;       // 32
+  int* flag;       // 32 deflated marks
+};
+
+__device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scratch S,
+                            double* lam, double* W, double* sW) {
+  const int lane = threadIdx.x & 31;
+  __shared__ int sh_K;
+  __shared__ double sh_wsum;
+  __shared__ double dwork[32];
+  // rotations basis
+  for (int i = lane; i < m * m; i += 32) {
+    const int a = i % m, b = i / m;
+    S.sQ[a * P + b] = (a == b) ? 1.0 : 0.0;
+  }
+  if (lane < m) {
+    dwork[lane] = d_in[lane];
+    S.zK[lane] = z_in[lane];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double zn2 = 0.0;
+    for (int i = 0; i < m; ++i) zn2 += S.zK[i] * S.zK[i];
+    const double zn = sqrt(zn2);
+    const double tol = 8.0 * DBL_EPSILON * (dwork[0] + zn2);
+    for (int i = 0; i < m; ++i) S.flag[i] = (fabs(S.zK[i]) * zn <= tol) ? 1 : 0;
+    // close poles: rotate the later coordinate's weight into the earlier one
+    int prev = -1;
+    for (int i = 0; i < m; ++i) {
+      if (S.flag[i]) continue;
+      if (prev >= 0) {
+        const double zp = S.zK[prev], zi = S.zK[i];
+        const double rr = hypot(zp, zi);
+        const double c = zp / rr, s = zi / rr;
+        if (fabs((dwork[prev] - dwork[i]) * c * s) <= tol) {
+          // G = [c s; -s c] on (prev, i): z_prev <- r, z_i <- 0
+          const double dp = dwork[prev], di = dwork[i];
+          dwork[prev] = c * c * dp + s * s * di;
+          dwork[i] = s * s * dp + c * c * di;
+          S.zK[prev] = rr;
+          S.zK[i] = 0.0;
+          for (int a = 0; a < m; ++a) {
+            const double qp = S.sQ[a * P + prev], qi = S.sQ[a * P + i];
+            S.sQ[a * P + prev] = c * qp + s * qi;
+            S.sQ[a * P + i] = -s * qp + c * qi;
+          }
+          S.flag[i] = 1;
+          continue;
+        }
+      }
+      prev = i;
+    }
+    int K = 0;
+    double wsum = 0.0;
+    for (int i = 0; i < m; ++i)
+      if (!S.flag[i]) {
+        S.idx[K] = i;
+        S.dK[K] = dwork[i];
+        S.wK[K] = S.zK[i] * S.zK[i];
+        wsum += S.wK[K];
+        ++K;
+      }
+    sh_K = K;
+    sh_wsum = wsum;
+  }
+  __syncwarp();
+  const int K = sh_K;
+  // roots
+  int iters = 0;
+  if (lane < K) {
+    int o;
+    double tau;
+    iters = solve_root(S.dK, S.wK, K, sh_wsum, lane, o, tau);
+    S.ls[lane] = S.dK[o];
+    S.lt[lane] = tau;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) iters = max(iters, __shfl_xor_sync(FULL, iters, off));
+  __syncwarp();
+  // Loewner z-hat: zh_i^2 = (l_i - d_i) prod_{j != i} (l_j - d_i) / (d_j - d_i)
+  if (lane < K) {
+    const int i = lane;
+    const double di = S.dK[i];
+    double prod = (S.ls[i] - di) + S.lt[i];
+    for (int j = 0; j < K; ++j) {
+      if (j == i) continue;
+      const double num = (S.ls[j] - di) + S.lt[j];
+      prod *= num * rcp(S.dK[j] - di);
+    }
+    const double zi = S.zK[S.idx[i]];
+    const double mag = sqrt(fabs(prod));
+    S.zh[i] = (zi < 0.0) ? -mag : mag;
+  }
+  __syncwarp();
+  // all eigenvalues (non-deflated roots then deflated poles) + sort
+  __shared__ int src_kind[32];
+  if (lane < m) {
+    // position lane: lanes < K are roots, the rest map to deflated coordinates
+    double lv;
+    if (lane < K) {
+      lv = S.ls[lane] + S.lt[lane];
+      src_kind[lane] = lane;  // root id
+    } else {
+      int cnt = 0, coord = 0;
+      for (int a = 0; a < m; ++a)
+        if (S.flag[a]) {
+          if (cnt == lane - K) {
+            coord = a;
+            break;
+          }
+          ++cnt;
+        }
+      lv = dwork[coord];
+      src_kind[lane] = 32 + coord;  // deflated coordinate
+    }
+    S.lamall[lane] = lv;
+  }
+  __syncwarp();
+  if (lane < m) {
+    const double li = S.lamall[lane];
+    int rk = 0;
+    for (int j = 0; j < m; ++j) {
+      const double lj = S.lamall[j];
+      if (lj > li || (lj == li && j < lane)) ++rk;
+    }
+    S.perm[rk] = lane;
+  }
+  __syncwarp();
+  // eigenvector columns (lane = output column), sign rule, clamp
+  if (lane < m) {
+    const int src = S.perm[lane];
+    const int kind = src_kind[src];
+    for (int a = 0; a < m; ++a) sW[a * P + lane] = 0.0;
+    if (kind < 32) {
+      const int j = kind;
+      double nrm2 = 0.0;
+      for (int i = 0; i < K; ++i) {
+        const double t = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]);
+        nrm2 += t * t;
+      }
+      const double inv = 1.0 / sqrt(nrm2);
+      for (int i = 0; i < K; ++i) {
+        const double c = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
+        const int coord = S.idx[i];
+        for (int a = 0; a < m; ++a) sW[a * P + lane] += S.sQ[a * P + coord] * c;
+      }
+    } else {
+      const int coord = kind - 32;
+      for (int a = 0; a < m; ++a) sW[a * P + lane] = S.sQ[a * P + coord];
+    }
+    int arg = 0;
+    double best = fabs(sW[lane]);
+    for (int a = 1; a < m; ++a) {
+      const double av = fabs(sW[a * P + lane]);
+      if (av > best) {
+        best = av;
+        arg = a;
+      }
+    }
+    const bool flip = sW[arg * P + lane] < 0.0;
+    for (int a = 0; a < m; ++a) {
+      const double v = flip ? -sW[a * P + lane] : sW[a * P + lane];
+      sW[a * P + lane] = v;
+      W[a + lane * m] = v;
+    }
+    const double lv = S.lamall[src];
+    lam[lane] = lv < 0.0 ? 0.0 : lv;
+  }
+  __syncwarp();
+  return iters;
+}
+
+}  // namespace secular
+}  // namespace tsg
