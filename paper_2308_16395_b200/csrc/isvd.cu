@@ -115,21 +115,23 @@ __device__ int inner_truncate(const InnerIO& io, double* lam, int m, int sweeps)
   } else {
     c->status = 3;  // S' == 0 cannot happen with r >= 1 and sigma > 0
   }
-  c->trunc_margin = margin;
-  c->sweeps = sweeps;
   double added = disc;
   if (io.deg) added += io.k * io.k;
+  const double sq_err = c->squared_error;
+  c->trunc_margin = margin;
+  c->sweeps = sweeps;
   c->added_error_sq = added;
-  c->squared_error += added;  // isvd.cpp:212-215
+  c->squared_error = sq_err + added;  // isvd.cpp:212-215
   c->r_new = rank;
   c->degenerate = io.deg;
   return rank;
 }
 
-// Whole inner problem in one warp (m = columns of S' <= 32). Shared-memory
-// scratch: G, V, U with pitch 33 (conflict-free), perm (ints).
-__device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sV, double* sU,
-                                 int* perm) {
+// Whole inner problem in one warp (m = columns of S' <= 32). RM >= r + 1
+// bounds the rows of S' so that MGS columns live in registers. Shared-memory
+// scratch: sG (sorted eigenvectors, pitch 33) and sU (left factor).
+template <int RM>
+__device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sU) {
   const int lane = threadIdx.x & 31;
   const int r = io.r;
   const int m = io.deg ? r : r + 1;
@@ -139,10 +141,12 @@ __device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sV, doub
   double* lam = io.inner + L.lam;
   double* W = io.inner + L.W;
   // S'^T S' = diag(s^2, 0) + z z^T, z = [p; k] (degenerate: diag(s^2) + p p^T)
-  __shared__ double sd[32], sz[32], sQ[32 * 33], sx[8 * 32];
+  __shared__ double sd[32], sz[33], ssig[32], sQ[32 * 33], sx[8 * 32];
   __shared__ int si[3 * 32];
   if (lane < m) {
-    sd[lane] = lane < r ? io.sigma[lane] * io.sigma[lane] : 0.0;
+    const double sg = lane < r ? io.sigma[lane] : 0.0;
+    ssig[lane] = sg;
+    sd[lane] = sg * sg;
     sz[lane] = lane < r ? io.p[lane] : io.k;
   }
   __syncwarp();
@@ -159,61 +163,75 @@ __device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sV, doub
   S.idx = si;
   S.perm = si + 32;
   S.flag = si + 64;
-  const int sweep = secular::eig_rank_one(m, sd, sz, S, lam, W, sG);
-  (void)sV;
-  (void)perm;
+  const int iters = secular::eig_rank_one(m, sd, sz, S, lam, W, sG);
   TSG_CLK(5);
   int rank = 0;
-  if (lane == 0) rank = inner_truncate(io, lam, m, sweep);
+  if (lane == 0) rank = inner_truncate(io, lam, m, iters);
   rank = __shfl_sync(FULL, rank, 0);
   __syncwarp();
   TSG_CLK(6);
-  // sigma_new, U = S' W / sigma (multiply, isvd.cpp:217; linalg.cpp:250-256)
+  // sigma_new and U = S' W / sigma, column `lane` in registers
+  // (multiply, linalg.cpp:250-256; rows i < r of S' are diag(s))
+  double u[RM];
+#pragma unroll
+  for (int l = 0; l < RM; ++l) u[l] = 0.0;
   if (lane < rank) {
-    io.sigma_new[lane] = sqrt(lam[lane]);
-    const double inv = 1.0 / sqrt(lam[lane]);
-    for (int i = 0; i < r; ++i) sU[i * P + lane] = io.sigma[i] * sG[i * P + lane] * inv;
+    const double lj = lam[lane];
+    io.sigma_new[lane] = sqrt(lj);
+    const double inv = 1.0 / sqrt(lj);
     double s = 0.0;
-    for (int l = 0; l < m; ++l) {
-      const double wl = sG[l * P + lane];
-      if (wl == 0.0) continue;
-      s += sz[l] * wl;
+    for (int l = 0; l < m; ++l) s += sz[l] * sG[l * P + lane];
+#pragma unroll
+    for (int l = 0; l < RM; ++l) {
+      if (l < r) u[l] = ssig[l] * sG[l * P + lane] * inv;
+      else if (l == r) u[l] = s * inv;
     }
-    sU[r * P + lane] = s * inv;
   }
-  __syncwarp();
+  // one MGS pass, right-looking (linalg.cpp:64-78); column i broadcast by shuffles
   for (int i = 0; i < rank; ++i) {
     if (lane == i) {
       double ss = 0.0;
-      for (int l = 0; l < rows; ++l) ss += sU[l * P + i] * sU[l * P + i];
+#pragma unroll
+      for (int l = 0; l < RM; ++l) ss += u[l] * u[l];
       const double nrm = sqrt(ss);
-      if (nrm > 0.0)
-        for (int l = 0; l < rows; ++l) sU[l * P + i] /= nrm;
+      if (nrm > 0.0) {
+#pragma unroll
+        for (int l = 0; l < RM; ++l) u[l] /= nrm;
+      }
     }
-    __syncwarp();
+    double dot = 0.0;
+    double ui[RM];
+#pragma unroll
+    for (int l = 0; l < RM; ++l) {
+      ui[l] = __shfl_sync(FULL, u[l], i);
+      dot += ui[l] * u[l];
+    }
     if (lane > i && lane < rank) {
-      double dot = 0.0;
-      for (int l = 0; l < rows; ++l) dot += sU[l * P + i] * sU[l * P + lane];
-      for (int l = 0; l < rows; ++l) sU[l * P + lane] -= dot * sU[l * P + i];
+#pragma unroll
+      for (int l = 0; l < RM; ++l) u[l] -= dot * ui[l];
     }
-    __syncwarp();
   }
   TSG_CLK(7);
   // outputs: U (P'), M = P'_top^T p_gram, w = last row of P'
   double* U = io.inner + L.U;
   double* M = io.inner + L.M;
   double* w = io.inner + L.w;
-  for (int idx = lane; idx < rows * rank; idx += 32) {
-    const int i = idx % rows, j = idx / rows;
-    U[i + j * rows] = sU[i * P + j];
+  if (lane < rank) {
+#pragma unroll
+    for (int l = 0; l < RM; ++l)
+      if (l < rows) {
+        sU[l * P + lane] = u[l];
+        U[l + lane * rows] = u[l];
+      }
+    w[lane] = sU[r * P + lane];
   }
+  __syncwarp();
   for (int idx = lane; idx < rank * r; idx += 32) {
     const int jn = idx % rank, j = idx / rank;
     double s = 0.0;
     for (int l = 0; l < r; ++l) s += sU[l * P + jn] * io.pgram[l + j * r];
     M[jn + j * rank] = s;
   }
-  if (lane < rank) w[lane] = sU[r * P + lane];
   __syncwarp();
 }
 
@@ -449,22 +467,35 @@ __device__ void pgram_block(const double* __restrict__ left, long long n_d, int 
 
 __device__ void finalize_record(Ctrl* c, double d, double cs, Metrics* rec, int order,
                                 const SpatialRanks& sr) {
+  // one batch of independent loads, then stores (no load-after-store chains)
+  const int r_new = c->r_new, status = c->status, sweeps = c->sweeps;
+  const long long n_d = c->n_d, ins = c->insertions;
+  const double slice_sq = c->slice_sq, proj_sq = c->proj_sq, margin = c->trunc_margin;
+  const double sq_err = c->squared_error, ns = c->nonstream_discarded_sq, tot = c->total_input_sq;
+  double res[kMaxD];
+#pragma unroll
+  for (int k = 0; k < kMaxD; ++k) res[k] = c->res_sq[k];
   c->coupling_diff_sq = d;
   c->core_sq = cs;
-  if (sqrt(d) > kCouplingTol * sqrt(cs) + 1e-300) c->status = 2;  // streaming.cpp:55-63
-  c->r = c->r_new;
-  rec->slice_index = c->n_d;
-  c->n_d += 1;
-  c->insertions += 1;
-  for (int k = 0; k + 1 < order; ++k) rec->ranks[k] = sr.v[k];
-  rec->ranks[order - 1] = c->r;
-  rec->slice_norm = sqrt(c->slice_sq);
-  rec->projected_norm = sqrt(c->proj_sq);
-  for (int k = 0; k + 1 < order; ++k) rec->mode_residuals[k] = sqrt(c->res_sq[k]);
-  const double booked = c->squared_error + c->nonstream_discarded_sq;
-  rec->error_estimate = c->total_input_sq <= 0.0 ? 0.0 : sqrt(fmax(booked, 0.0) / c->total_input_sq);
-  rec->trunc_margin = c->trunc_margin;
-  rec->sweeps = c->sweeps;
+  if (sqrt(d) > kCouplingTol * sqrt(cs) + 1e-300 && status == 0) c->status = 2;  // streaming.cpp:55-63
+  c->r = r_new;
+  c->n_d = n_d + 1;
+  c->insertions = ins + 1;
+  Metrics m;
+  m.slice_index = n_d;
+#pragma unroll
+  for (int k = 0; k < kMaxD; ++k) m.ranks[k] = (k + 1 < order) ? sr.v[k] : 0;
+  m.ranks[order - 1] = r_new;
+  m.slice_norm = sqrt(slice_sq);
+  m.projected_norm = sqrt(proj_sq);
+#pragma unroll
+  for (int k = 0; k < kMaxD; ++k) m.mode_residuals[k] = (k + 1 < order) ? sqrt(res[k]) : 0.0;
+  const double booked = sq_err + ns;
+  m.error_estimate = tot <= 0.0 ? 0.0 : sqrt(fmax(booked, 0.0) / tot);
+  m.expanded_mask = 0;
+  m.trunc_margin = margin;
+  m.sweeps = sweeps;
+  *rec = m;
 }
 
 // Row update of Q and the core for rows [i0, i1): Qn = [Q q] W,
@@ -590,41 +621,64 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
   double* sV = sG + 32 * 33;
   double* sU = sV + 32 * 33;
   TSG_CLK(0);
-  // p_gram (old left) and p1 = Q^T b, ||b||^2
+  // p_gram (old left) for the core rotation
   pgram_block(B.left, B.n_d, B.capr, r, pg);
-  for (int j = wid; j < r; j += 16) {
-    const double* qj = B.q + (long long)j * n;
-    double s = 0.0;
-#pragma unroll 4
-    for (long long i = lane; i < n; i += 32) s += qj[i] * B.b[i];
-    s = warp_sum(s);
-    if (lane == 0) sp1[j] = s;
-  }
-  double bs = 0.0;
-  for (long long i = threadIdx.x; i < n; i += blockDim.x) bs += B.b[i] * B.b[i];
-  bs = block_sum(bs, red);  // includes __syncthreads
-  // e1 = b - Q p1
+  __syncthreads();
+  TSG_CLK(8);
+  // Two classical Gram-Schmidt passes (CGS2) split b = Q p + e
+  // (isvd.cpp:172-191 uses two MGS passes: same projector, parallel form).
+  // Row-parallel: each thread accumulates all r dot products of its rows.
+  __shared__ double wpart[16][RMAX + 1];
+  const double* __restrict__ q = B.q;
+  const double* __restrict__ bv = B.b;
+  auto reduce_to = [&](double (&acc)[RMAX + 1], double* dst, int cnt) {
+#pragma unroll
+    for (int j = 0; j <= RMAX; ++j) {
+      const double v = warp_sum(acc[j]);
+      if (lane == 0) wpart[wid][j] = v;
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < cnt; j += blockDim.x) {
+      double s = 0.0;
+      for (int w = 0; w < 16; ++w) s += wpart[w][j];
+      dst[j] = s;
+    }
+    __syncthreads();
+  };
+  double acc[RMAX + 1];
+#pragma unroll
+  for (int j = 0; j <= RMAX; ++j) acc[j] = 0.0;
   for (long long i = threadIdx.x; i < n; i += blockDim.x) {
-    double s = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < r; ++j) s += B.q[i + (long long)j * n] * sp1[j];
-    se[i] = B.b[i] - s;
+    const double bi = bv[i];
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j)
+      if (j < r) acc[j] += q[i + (long long)j * n] * bi;
+    acc[RMAX] += bi * bi;
   }
-  __syncthreads();
-  for (int j = wid; j < r; j += 16) {
-    const double* qj = B.q + (long long)j * n;
+  reduce_to(acc, sp1, RMAX + 1);
+  const double bs = sp1[RMAX];
+#pragma unroll
+  for (int j = 0; j <= RMAX; ++j) acc[j] = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) {
+    double qr[RMAX];
     double s = 0.0;
-#pragma unroll 4
-    for (long long i = lane; i < n; i += 32) s += qj[i] * se[i];
-    s = warp_sum(s);
-    if (lane == 0) sp2[j] = s;
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) {
+      qr[j] = j < r ? q[i + (long long)j * n] : 0.0;
+      s += qr[j] * sp1[j];
+    }
+    const double e1 = bv[i] - s;
+    se[i] = e1;
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j) acc[j] += qr[j] * e1;
   }
-  __syncthreads();
+  reduce_to(acc, sp2, RMAX);
   double es = 0.0;
   for (long long i = threadIdx.x; i < n; i += blockDim.x) {
     double s = 0.0;
-#pragma unroll 4
-    for (int j = 0; j < r; ++j) s += B.q[i + (long long)j * n] * sp2[j];
+#pragma unroll
+    for (int j = 0; j < RMAX; ++j)
+      if (j < r) s += q[i + (long long)j * n] * sp2[j];
     const double v = se[i] - s;
     se[i] = v;
     es += v * v;
@@ -653,7 +707,7 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
     io.inner = B.inner;
     io.sigma_new = B.sigma_new;
     io.capr = B.capr;
-    inner_solve_warp(io, sG, sV, sU, sperm);
+    inner_solve_warp<RMAX + 1>(io, sG, sU);
   }
   __syncthreads();
   TSG_CLK(2);
@@ -683,6 +737,7 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
     SpatialRanks sr;
     for (int k = 0; k < kMaxD; ++k) sr.v[k] = B.spatial_ranks[k];
     finalize_record(c, dacc, cacc, B.metrics, B.order, sr);
+    TSG_CLK(9);
   }
 }
 
@@ -837,7 +892,7 @@ __global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
   if (m <= 32) {
     if (threadIdx.x < 32) {
       double* sG = ism;
-      inner_solve_warp(io, sG, sG + 32 * 33, sG + 64 * 33, sperm);
+      inner_solve_warp<33>(io, sG, sG + 64 * 33);
     }
   } else {
     double* G = a.use_smem ? ism : a.inner + L.G;

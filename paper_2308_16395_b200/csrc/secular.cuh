@@ -133,7 +133,7 @@ struct Scratch {
 __device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scratch S,
                             double* lam, double* W, double* sW) {
   const int lane = threadIdx.x & 31;
-  __shared__ int sh_K;
+  __shared__ int sh_K, sh_rot;
   __shared__ double sh_wsum;
   __shared__ double dwork[32];
   // rotations basis
@@ -153,14 +153,18 @@ __device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scrat
     const double tol = 8.0 * DBL_EPSILON * (dwork[0] + zn2);
     for (int i = 0; i < m; ++i) S.flag[i] = (fabs(S.zK[i]) * zn <= tol) ? 1 : 0;
     // close poles: rotate the later coordinate's weight into the earlier one
-    int prev = -1;
+    int prev = -1, rotated = 0;
     for (int i = 0; i < m; ++i) {
       if (S.flag[i]) continue;
-      if (prev >= 0) {
+      // |(d_p - d_i) c s| <= tol with c s = z_p z_i / (z_p^2 + z_i^2), tested
+      // without the square root first
+      if (prev >= 0 && fabs(dwork[prev] - dwork[i]) * fabs(S.zK[prev] * S.zK[i]) <=
+                           tol * (S.zK[prev] * S.zK[prev] + S.zK[i] * S.zK[i])) {
         const double zp = S.zK[prev], zi = S.zK[i];
         const double rr = hypot(zp, zi);
         const double c = zp / rr, s = zi / rr;
-        if (fabs((dwork[prev] - dwork[i]) * c * s) <= tol) {
+        {
+          rotated = 1;
           // G = [c s; -s c] on (prev, i): z_prev <- r, z_i <- 0
           const double dp = dwork[prev], di = dwork[i];
           dwork[prev] = c * c * dp + s * s * di;
@@ -190,6 +194,7 @@ __device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scrat
       }
     sh_K = K;
     sh_wsum = wsum;
+    sh_rot = rotated;
   }
   __syncwarp();
   const int K = sh_K;
@@ -267,10 +272,15 @@ __device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scrat
         nrm2 += t * t;
       }
       const double inv = 1.0 / sqrt(nrm2);
-      for (int i = 0; i < K; ++i) {
-        const double c = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
-        const int coord = S.idx[i];
-        for (int a = 0; a < m; ++a) sW[a * P + lane] += S.sQ[a * P + coord] * c;
+      if (!sh_rot) {
+        for (int i = 0; i < K; ++i)
+          sW[S.idx[i] * P + lane] = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
+      } else {
+        for (int i = 0; i < K; ++i) {
+          const double c = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
+          const int coord = S.idx[i];
+          for (int a = 0; a < m; ++a) sW[a * P + lane] += S.sQ[a * P + coord] * c;
+        }
       }
     } else {
       const int coord = kind - 32;
