@@ -22,10 +22,7 @@ struct Ctrl {
   double squared_error;
   double total_input_sq;
   double nonstream_discarded_sq;
-  // per-slice scalars
-  double slice_sq;      // ||y||^2
-  double delta;         // tau ||y|| / sqrt(d)
-  double res_sq[kMaxD]; // ||E_k||^2 per non-streaming mode
+  // per-insertion scalars (ISVD stream)
   double proj_sq;       // ||b||^2, b = vec(projected slice)
   double e_sq;          // ||e||^2 after the two projection passes
   double added_error_sq;
@@ -34,10 +31,17 @@ struct Ctrl {
   long long n_d, insertions;
   int r, r_new, degenerate;
   int status;           // 0 ok, 2 coupling drift, 3 numerical
+  int sweeps;
+};
+
+// Per-slice decision record, written by the projection stream and read by
+// the ISVD stream, so consecutive slices can be in flight at once.
+struct SliceCtl {
+  double slice_sq;      // ||y||^2
+  double delta;         // tau ||y|| / sqrt(d)  (streaming.cpp:187-188)
+  double res_sq[kMaxD]; // ||E_k||^2 per non-streaming mode
   int expand_mode;      // first mode whose residual exceeds delta, -1 none
   int zero_slice;
-  int sweeps;
-  int pad_;
 };
 
 struct Metrics {  // mirrors tsg_slice_metrics' device-filled part

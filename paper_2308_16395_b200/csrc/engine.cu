@@ -89,15 +89,34 @@ struct tsg_stream {
   long long ipart_cap = 0;
   double* pgram = nullptr;
   double* inner = nullptr;
+  unsigned* tile_ctr = nullptr;  // dynamic tile-scheduler counters
+  unsigned ctr_next = 0;
   Ctrl* ctrl = nullptr;
   Ctrl* ctrl_h = nullptr;
-  Metrics* mdev = nullptr;
-  Metrics* mhost = nullptr;
-  int mslot = 0;
-  bool pending = false;       // an ISVD record not yet drained
-  int pending_slot = 0;
-  int pending_mask = 0;
-  double pending_wall = 0.0;
+  // two-stage pipeline: projections of slice t+1 (stream st) overlap the
+  // ISVD of slice t (stream si); per-parity decision slots and work buffers
+  cudaStream_t si = nullptr;
+  SliceCtl* slots = nullptr;     // device [2]
+  SliceCtl* slots_h = nullptr;   // pinned mirror [2]
+  double* pw[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  long long pipe_elems = 0;
+  cudaEvent_t ev_proj[2] = {nullptr, nullptr}, ev_isvd[2] = {nullptr, nullptr};
+  bool ev_isvd_valid[2] = {false, false};
+  long long upd_count = 0;
+  // metrics ring: each insertion writes one record + a ctrl snapshot
+  static constexpr int kRing = 8;
+  Metrics* mdev = nullptr;       // device [kRing]
+  Metrics* mhost = nullptr;      // pinned [kRing]
+  Ctrl* cring_h = nullptr;       // pinned [kRing] ctrl snapshots
+  cudaEvent_t ev_rec[kRing] = {};
+  struct Pending {
+    int slot, mask;
+    double wall;
+  };
+  std::vector<Pending> pending;  // FIFO, oldest first
+  int ring_next = 0;
+  int r_exact = 0;               // streaming rank after the last drained insertion
+  int drift_pending = 0;
   std::vector<tsg_slice_metrics> metrics;
 
   // phase profiling (TSG_PROFILE)
@@ -116,10 +135,10 @@ struct tsg_stream {
     ev_pool.pop_back();
     return e;
   }
-  void ev_mark(int i) {
+  void ev_mark(int i, cudaStream_t s_) {
     if (!profiling()) return;
     ev_cur[i] = ev_get();
-    ck(cudaEventRecord(ev_cur[i], st), "cudaEventRecord");
+    ck(cudaEventRecord(ev_cur[i], s_), "cudaEventRecord");
   }
   void ev_commit() {
     if (!profiling()) return;
@@ -168,16 +187,26 @@ struct tsg_stream {
     cudaFree(p);
   }
   void free_all() {
+    if (st) cudaStreamSynchronize(st);
+    if (si) cudaStreamSynchronize(si);
     for (auto& a : allocs) cudaFree(a.first);
     allocs.clear();
     cur_bytes = 0;
     if (ctrl_h) cudaFreeHost(ctrl_h);
     if (mhost) cudaFreeHost(mhost);
+    if (cring_h) cudaFreeHost(cring_h);
+    if (slots_h) cudaFreeHost(slots_h);
     ctrl_h = nullptr;
     mhost = nullptr;
+    cring_h = nullptr;
+    slots_h = nullptr;
   }
 
-  void sync() { ck(cudaStreamSynchronize(st), "cudaStreamSynchronize"); }
+  // both streams
+  void sync() {
+    ck(cudaStreamSynchronize(si), "cudaStreamSynchronize");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+  }
   // TSG_DEBUG_SYNC=1: synchronise and check after each orchestration step.
   bool debug_sync = std::getenv("TSG_DEBUG_SYNC") != nullptr;
   void dbg(const char* where) {
@@ -187,10 +216,18 @@ struct tsg_stream {
   }
 
   void pull_ctrl() {
+    ck(cudaStreamSynchronize(si), "cudaStreamSynchronize");
     ck(cudaMemcpyAsync(ctrl_h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
     sync();
     ck(cudaGetLastError(), "kernel");
     if (!ev_pending.empty()) ev_resolve();
+  }
+  // this slice's decision record (projection stream only)
+  void pull_slot(int par) {
+    ck(cudaMemcpyAsync(slots_h + par, slots + par, sizeof(SliceCtl), cudaMemcpyDeviceToHost, st),
+       "slot D2H");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "kernel");
   }
   void push_ctrl() {
     ck(cudaMemcpyAsync(ctrl, ctrl_h, sizeof(Ctrl), cudaMemcpyHostToDevice, st), "ctrl H2D");
@@ -261,30 +298,45 @@ struct tsg_stream {
   }
 
   // ---------------------------------------------------- metrics drain
-  void drain() {
-    if (!pending) return;
-    ck(cudaMemcpyAsync(mhost + pending_slot, mdev + pending_slot, sizeof(Metrics),
-                       cudaMemcpyDeviceToHost, st), "metrics D2H");
-    sync();
-    const Metrics& m = mhost[pending_slot];
-    tsg_slice_metrics o;
-    std::memset(&o, 0, sizeof o);
-    o.slice_index = m.slice_index;
-    for (int k = 0; k < d; ++k) o.ranks[k] = m.ranks[k];
-    o.slice_norm = m.slice_norm;
-    o.projected_norm = m.projected_norm;
-    o.error_estimate = m.error_estimate;
-    for (int k = 0; k + 1 < d; ++k) o.mode_residuals[k] = m.mode_residuals[k];
-    o.expanded_mask = pending_mask;
-    o.peak_bytes = peak_bytes;
-    o.wall_ms = pending_wall;
-    o.trunc_margin = m.trunc_margin;
-    o.jacobi_sweeps = m.sweeps;
-    metrics.push_back(o);
-    pending = false;
+  // Retire finished insertions in order (all of them when `force`).
+  void drain(bool force = true) {
+    while (!pending.empty()) {
+      const Pending p = pending.front();
+      if (force) {
+        ck(cudaEventSynchronize(ev_rec[p.slot]), "cudaEventSynchronize");
+      } else if (cudaEventQuery(ev_rec[p.slot]) != cudaSuccess) {
+        break;
+      }
+      const Metrics& m = mhost[p.slot];
+      tsg_slice_metrics o;
+      std::memset(&o, 0, sizeof o);
+      o.slice_index = m.slice_index;
+      for (int k = 0; k < d; ++k) o.ranks[k] = m.ranks[k];
+      o.slice_norm = m.slice_norm;
+      o.projected_norm = m.projected_norm;
+      o.error_estimate = m.error_estimate;
+      for (int k = 0; k + 1 < d; ++k) o.mode_residuals[k] = m.mode_residuals[k];
+      o.expanded_mask = p.mask;
+      o.peak_bytes = peak_bytes;
+      o.wall_ms = p.wall;
+      o.trunc_margin = m.trunc_margin;
+      o.jacobi_sweeps = m.sweeps;
+      metrics.push_back(o);
+      r_exact = cring_h[p.slot].r;
+      if (cring_h[p.slot].status != 0) drift_pending = cring_h[p.slot].status;
+      pending.erase(pending.begin());
+    }
   }
 
   void check_status() {
+    if (drift_pending) {
+      const int code = drift_pending;
+      drift_pending = 0;
+      if (code == 2)
+        fail(TSG_EDRIFT,
+             "streaming state invariant violated: core no longer matches the ISVD factorization");
+      fail(TSG_EOTHER, "device numerical failure");
+    }
     if (ctrl_h->status == 2)
       fail(TSG_EDRIFT,
            "streaming state invariant violated: core no longer matches the ISVD factorization");
@@ -384,6 +436,9 @@ struct tsg_stream {
     a.partial = part;
     a.residual = 1;
     a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? 1 : 0;
+    if (!tile_ctr) tile_ctr = reinterpret_cast<unsigned*>(dalloc(kMaxD * 2));
+    a.tile_counter = tile_ctr + (ctr_next++ % (kMaxD * 4));
+    ck(cudaMemsetAsync(a.tile_counter, 0, sizeof(unsigned), st), "memset");
     return launch_project(a, st);
   }
 
@@ -473,76 +528,202 @@ struct tsg_stream {
     return nullptr;
   }
 
+  // Work buffers of the pipelined path: two per slice parity, sized for the
+  // largest projected tensor (the output of mode 0).
+  void ensure_pipe() {
+    long long need = 1;
+    for (int k = 0; k + 1 < d; ++k) need *= (k == 0 ? R[0] : N[k]);
+    if (need <= pipe_elems) return;
+    sync();
+    for (auto& set : pw)
+      for (auto& b : set) {
+        dfree(b);
+        b = dalloc(need);
+      }
+    pipe_elems = need;
+  }
+
+  // Enqueue the ISVD insertion + core rotation for the slice whose projected
+  // tensor is `b` and whose decisions are in slot `par`, on stream `s_`.
+  void enqueue_isvd(const double* b, int par, int mask, cudaStream_t s_, bool commit,
+                    std::chrono::steady_clock::time_point t0) {
+    drain(false);
+    int r_ub = r_exact + (int)pending.size();
+    if (r_ub + 1 > capr) {
+      sync();
+      drain(true);
+      r_ub = r_exact;
+      if (r_ub + 1 > capr) grow_capr(std::max(capr + 16, (r_ub + 1 + 7) / 8 * 8 + 8));
+    }
+    if (n_d + 1 > cap_rows) {
+      sync();
+      grow_rows(n_d + 1);
+    }
+    const long long n = n_rows();
+    if (evec_n < n) {
+      sync();
+      dfree(evec);
+      evec = dalloc(n);
+      evec_n = n;
+    }
+    // metrics ring slot: wait for its previous owner to retire
+    const int ms = ring_next;
+    ring_next = (ring_next + 1) % kRing;
+    for (const Pending& p : pending)
+      if (p.slot == ms) {
+        drain(true);
+        break;
+      }
+    if (s_ != st) ck(cudaStreamWaitEvent(s_, ev_proj[par], 0), "cudaStreamWaitEvent");
+    if (commit) launch_commit_modes(ctrl, slots + par, 0, d - 1, 1, s_);
+    IsvdBufs B;
+    std::memset(&B, 0, sizeof B);
+    B.ctrl = ctrl;
+    B.slot = slots + par;
+    B.b = b;
+    B.q = Q;
+    B.qn = Q2;
+    B.c = core;
+    B.cn = core2;
+    B.e = evec;
+    B.sigma = sigma;
+    B.sigma_new = sigma2;
+    B.left = left;
+    B.left_new = left2;
+    B.pgram = pgram;
+    B.inner = inner;
+    B.partial = ipart;
+    B.metrics = mdev + ms;
+    B.n = n;
+    B.n_d = n_d;
+    B.capr = capr;
+    B.order = d;
+    B.r_hint = r_ub;
+    for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
+    ev_mark(3, s_);
+    launch_isvd(B, s_);
+    ev_mark(4, s_);
+    if (mask == 0) ev_commit();
+    ck(cudaMemcpyAsync(cring_h + ms, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s_), "ctrl D2H");
+    ck(cudaMemcpyAsync(mhost + ms, mdev + ms, sizeof(Metrics), cudaMemcpyDeviceToHost, s_),
+       "metrics D2H");
+    ck(cudaEventRecord(ev_rec[ms], s_), "cudaEventRecord");
+    ck(cudaEventRecord(ev_isvd[par], s_), "cudaEventRecord");
+    ev_isvd_valid[par] = true;
+    std::swap(Q, Q2);
+    std::swap(core, core2);
+    std::swap(sigma, sigma2);
+    std::swap(left, left2);
+    ++n_d;
+    ++insertions_host;
+    pending.push_back(Pending{ms, mask,
+                              std::chrono::duration<double, std::milli>(
+                                  std::chrono::steady_clock::now() - t0).count()});
+  }
+
   void update(const double* y_in, int mem_kind) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
+    const int par = (int)(upd_count++ & 1);
     const double* y = y_in;
     if (mem_kind == TSG_MEM_HOST) {
       ck(cudaMemcpyAsync(slice, y_in, sizeof(double) * slice_elems, cudaMemcpyHostToDevice, st),
          "slice H2D");
       y = slice;
     }
-    // Speculatively project every remaining mode from `base` (the input of
-    // mode m0), decide once, and on a residual above delta rebuild the
-    // expanding mode's input from `base`, grow the basis and continue.
+    ensure_pipe();
+    // this parity's buffers were last read by the insertion two slices ago
+    if (ev_isvd_valid[par]) ck(cudaStreamWaitEvent(st, ev_isvd[par], 0), "cudaStreamWaitEvent");
     long long yd[kMaxD];
     for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
     DecideArgs da;
     std::memset(&da, 0, sizeof da);
-    da.ctrl = ctrl;
+    da.slot = slots + par;
     da.nmodes = d - 1;
     da.tau = tau;
     da.order = d;
     da.partial = partial;
-    const double* base = y;
-    const double* b = nullptr;
-    int m0 = 0;
-    int mask = 0;
-    double delta = 0.0;
-    while (true) {
-      long long ydk[kMaxD];
-      std::memcpy(ydk, yd, sizeof yd);
-      const double* cur = base;
-      int off = 0;
-      for (int k = m0; k + 1 < d; ++k) {
-        double* out = pick(cur, base);
-        da.off[k] = off;
-        if (k == 0) ev_mark(0);
-        da.cnt[k] = project(cur, ydk, k, out, partial + off);
-        if (k == 0) ev_mark(1);
-        off += 2 * da.cnt[k];
-        ydk[k] = R[k];
-        cur = out;
-      }
-      da.first_mode = m0;
-      launch_decide(da, st);
-      if (m0 == 0) ev_mark(2);
-      if (m0 == 0) drain_async_pending();
+    const double* cur = y;
+    int off = 0;
+    for (int k = 0; k + 1 < d; ++k) {
+      double* out = pw[par][k & 1];
+      da.off[k] = off;
+      if (k == 0) ev_mark(0, st);
+      da.cnt[k] = project(cur, yd, k, out, partial + off);
+      if (k == 0) ev_mark(1, st);
+      off += 2 * da.cnt[k];
+      yd[k] = R[k];
+      cur = out;
+    }
+    da.first_mode = 0;
+    launch_decide(da, st);
+    ev_mark(2, st);
+    ck(cudaMemcpyAsync(slots_h + par, slots + par, sizeof(SliceCtl), cudaMemcpyDeviceToHost, st),
+       "slot D2H");
+    ck(cudaEventRecord(ev_proj[par], st), "cudaEventRecord");
+    // the previous slice's insertion keeps running on si meanwhile
+    ck(cudaEventSynchronize(ev_proj[par]), "cudaEventSynchronize");
+    ck(cudaGetLastError(), "kernel");
+    const SliceCtl& sc = slots_h[par];
+    if (sc.zero_slice || sc.expand_mode >= 0) {
+      update_slow(y, par, t0);
+    } else {
+      enqueue_isvd(cur, par, 0, si, true, t0);
+    }
+    if (!(flags & TSG_ASYNC)) {
+      drain(true);
       pull_ctrl();
       check_status();
-      if (m0 == 0) {
-        r_host = ctrl_h->r;
-        delta = ctrl_h->delta;
-        if (ctrl_h->zero_slice) {
-          launch_commit_modes(ctrl, 0, 0, 1, st);
-          grow_rows(n_d + 1);
-          long long sp[kMaxD] = {0};
-          for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
-          launch_zero_slice(ctrl, left, capr, mdev + mslot, d, sp, st);
-          ++n_d;
-          finish(t0, 0);
-          return;
-        }
-      }
-      const int em = ctrl_h->expand_mode;
-      if (em < 0) {
-        launch_commit_modes(ctrl, m0, d - 1, m0 == 0, st);
-        b = cur;
-        break;
-      }
-      launch_commit_modes(ctrl, m0, em, m0 == 0, st);
-      // rebuild the input of mode em (bitwise identical: same kernels, same data)
-      cur = base;
+    }
+  }
+
+  // Zero slice or basis growth: serialise both streams and run the
+  // host-orchestrated path (streaming.cpp:171-185, 140-151).
+  void update_slow(const double* y, int par, std::chrono::steady_clock::time_point t0) {
+    sync();
+    drain(true);
+    pull_ctrl();
+    const SliceCtl sc = slots_h[par];
+    if (sc.zero_slice) {
+      launch_commit_modes(ctrl, slots + par, 0, 0, 1, st);
+      if (n_d + 1 > cap_rows) grow_rows(n_d + 1);
+      const int ms = ring_next;
+      ring_next = (ring_next + 1) % kRing;
+      long long sp[kMaxD] = {0};
+      for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
+      launch_zero_slice(ctrl, left, capr, mdev + ms, d, sp, st);
+      ck(cudaMemcpyAsync(cring_h + ms, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
+      ck(cudaMemcpyAsync(mhost + ms, mdev + ms, sizeof(Metrics), cudaMemcpyDeviceToHost, st),
+         "metrics D2H");
+      ck(cudaEventRecord(ev_rec[ms], st), "cudaEventRecord");
+      ck(cudaEventRecord(ev_isvd[par], st), "cudaEventRecord");
+      ev_isvd_valid[par] = true;
+      ++n_d;
+      pending.push_back(Pending{ms, 0,
+                                std::chrono::duration<double, std::milli>(
+                                    std::chrono::steady_clock::now() - t0).count()});
+      return;
+    }
+    // Re-project from `base` (the input of mode m0), grow the first mode whose
+    // residual exceeds delta, continue with the grown tensor.
+    long long yd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+    DecideArgs da;
+    std::memset(&da, 0, sizeof da);
+    da.slot = slots + par;
+    da.nmodes = d - 1;
+    da.tau = tau;
+    da.order = d;
+    da.partial = partial;
+    const double delta = sc.delta;
+    int em = sc.expand_mode;
+    const double* base = y;
+    int m0 = 0, mask = 0;
+    launch_commit_modes(ctrl, slots + par, 0, em, 1, st);
+    const double* b = nullptr;
+    while (true) {
+      // rebuild the input of mode em from `base` (same kernels, same data)
+      const double* cur = base;
       for (int k = m0; k < em; ++k) {
         double* out = pick(cur, base);
         project(cur, yd, k, out, partial + 2LL * 148 * kMaxD);
@@ -559,79 +740,42 @@ struct tsg_stream {
         b = base;
         break;
       }
+      // speculatively project the remaining modes, decide once
+      long long ydk[kMaxD];
+      std::memcpy(ydk, yd, sizeof yd);
+      const double* c2 = base;
+      int off = 0;
+      for (int k = m0; k + 1 < d; ++k) {
+        double* out = pick(c2, base);
+        da.off[k] = off;
+        da.cnt[k] = project(c2, ydk, k, out, partial + off);
+        off += 2 * da.cnt[k];
+        ydk[k] = R[k];
+        c2 = out;
+      }
+      da.first_mode = m0;
+      launch_decide(da, st);
+      pull_slot(par);
+      em = slots_h[par].expand_mode;
+      if (em < 0) {
+        launch_commit_modes(ctrl, slots + par, m0, d - 1, 0, st);
+        b = c2;
+        break;
+      }
+      launch_commit_modes(ctrl, slots + par, m0, em, 0, st);
     }
-    const double* cur = b;
-    // ----- ISVD row insertion + core rotation (isvd.cpp:163-250, streaming.cpp:196-224)
-    const int r = ctrl_h->r;
-    if (r + 1 > capr) grow_capr(std::max(capr + 16, (r + 1 + 7) / 8 * 8 + 8));
-    grow_rows(n_d + 1);
-    const long long n = n_rows();
-    if (evec_n < n) {
-      dfree(evec);
-      evec = dalloc(n);
-      evec_n = n;
-    }
-    IsvdBufs B;
-    std::memset(&B, 0, sizeof B);
-    B.ctrl = ctrl;
-    B.b = cur;
-    B.q = Q;
-    B.qn = Q2;
-    B.c = core;
-    B.cn = core2;
-    B.e = evec;
-    B.sigma = sigma;
-    B.sigma_new = sigma2;
-    B.left = left;
-    B.left_new = left2;
-    B.pgram = pgram;
-    B.inner = inner;
-    B.partial = ipart;
-    B.metrics = mdev + mslot;
-    B.n = n;
-    B.n_d = n_d;
-    B.capr = capr;
-    B.order = d;
-    B.r_hint = r;
-    for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
-    ev_mark(3);
-    launch_isvd(B, st);
-    ev_mark(4);
-    if (mask == 0) ev_commit();
-    std::swap(Q, Q2);
-    std::swap(core, core2);
-    std::swap(sigma, sigma2);
-    std::swap(left, left2);
-    ++n_d;
-    ++insertions_host;
-    finish(t0, mask);
-  }
-
-  void finish(std::chrono::steady_clock::time_point t0, int mask) {
-    pending = true;
-    pending_slot = mslot;
-    pending_mask = mask;
-    mslot ^= 1;
-    if (!(flags & TSG_ASYNC)) {
-      pull_ctrl();
-      r_host = ctrl_h->r;
-      pending_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-      drain();
-      check_status();
-    } else {
-      pending_wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    }
-  }
-  // In async mode the previous record is complete once this slice's
-  // projections are (same stream); fetch it with the ctrl block.
-  void drain_async_pending() {
-    if (pending) drain();
+    pull_ctrl();
+    r_exact = ctrl_h->r;
+    ensure_pipe();
+    enqueue_isvd(b, par, mask, st, false, t0);
+    ck(cudaEventRecord(ev_proj[par], st), "cudaEventRecord");
   }
 
   void flush() {
-    drain();
+    sync();
+    drain(true);
     pull_ctrl();
-    r_host = ctrl_h->r;
+    r_exact = ctrl_h->r;
     check_status();
   }
 
@@ -750,7 +894,6 @@ struct tsg_stream {
     ctrl_h->nonstream_discarded_sq = 0.0;
     ctrl_h->r = r;
     ctrl_h->n_d = n_d;
-    ctrl_h->expand_mode = -1;
     push_ctrl();
     launch_coupling_check(ctrl, core, Q, sigma, n, r, nullptr, st);
     double defects[2];
@@ -764,6 +907,7 @@ struct tsg_stream {
     release(last);
     for (int k = order - 1; k < kMaxD; ++k) R[k] = 0;
     r_host = r;
+    r_exact = r;
     if (defects[0] > 1e-6) fail(TSG_EINVAL, "isvd_init: left factor not orthonormal");
     if (defects[1] > 1e-6) fail(TSG_EINVAL, "isvd_init: right factor not orthonormal");
     for (int j = 0; j < r; ++j) {
@@ -782,20 +926,51 @@ struct tsg_stream {
     for (int k = 0; k < kMaxD; ++k) U[k] = nullptr;
     core = core2 = Q = Q2 = sigma = sigma2 = left = left2 = nullptr;
     slice = slice_b = w0 = w1 = w2 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
+    tile_ctr = nullptr;
     partial_cap = ipart_cap = 0;
     evec_n = 0;
     metrics.clear();
-    pending = false;
-    mslot = 0;
+    pending.clear();
+    ring_next = 0;
+    r_exact = 0;
+    drift_pending = 0;
+    upd_count = 0;
+    ev_isvd_valid[0] = ev_isvd_valid[1] = false;
+    pipe_elems = 0;
+    for (auto& set : pw)
+      for (auto& b : set) b = nullptr;
     initialized = false;
     n_d = 0;
     insertions_host = 0;
+    if (!si) ck(cudaStreamCreateWithFlags(&si, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+      if (!ev_proj[i]) ck(cudaEventCreateWithFlags(&ev_proj[i], cudaEventDisableTiming), "event");
+      if (!ev_isvd[i]) ck(cudaEventCreateWithFlags(&ev_isvd[i], cudaEventDisableTiming), "event");
+    }
+    for (int i = 0; i < kRing; ++i)
+      if (!ev_rec[i]) ck(cudaEventCreateWithFlags(&ev_rec[i], cudaEventDisableTiming), "event");
     ctrl = reinterpret_cast<Ctrl*>(dalloc((sizeof(Ctrl) + 7) / 8));
     ck(cudaMallocHost(&ctrl_h, sizeof(Ctrl)), "cudaMallocHost");
     std::memset(ctrl_h, 0, sizeof(Ctrl));
     push_ctrl();
-    mdev = reinterpret_cast<Metrics*>(dalloc(2 * ((sizeof(Metrics) + 7) / 8)));
-    ck(cudaMallocHost(&mhost, 2 * sizeof(Metrics)), "cudaMallocHost");
+    slots = reinterpret_cast<SliceCtl*>(dalloc(2 * ((sizeof(SliceCtl) + 7) / 8)));
+    ck(cudaMallocHost(&slots_h, 2 * sizeof(SliceCtl)), "cudaMallocHost");
+    std::memset(slots_h, 0, 2 * sizeof(SliceCtl));
+    mdev = reinterpret_cast<Metrics*>(dalloc(kRing * ((sizeof(Metrics) + 7) / 8)));
+    ck(cudaMallocHost(&mhost, kRing * sizeof(Metrics)), "cudaMallocHost");
+    ck(cudaMallocHost(&cring_h, kRing * sizeof(Ctrl)), "cudaMallocHost");
+  }
+
+  void destroy_streams() {
+    for (int i = 0; i < 2; ++i) {
+      if (ev_proj[i]) cudaEventDestroy(ev_proj[i]);
+      if (ev_isvd[i]) cudaEventDestroy(ev_isvd[i]);
+    }
+    for (auto& e : ev_rec)
+      if (e) cudaEventDestroy(e);
+    for (auto e : ev_pool) cudaEventDestroy(e);
+    if (si) cudaStreamDestroy(si);
+    si = nullptr;
   }
 
   // ------------------------------------------------------ export/import
@@ -891,11 +1066,11 @@ struct tsg_stream {
     ctrl_h->r = r;
     ctrl_h->n_d = n_d;
     ctrl_h->insertions = dm->insertions;
-    ctrl_h->expand_mode = -1;
     push_ctrl();
     launch_coupling_check(ctrl, core, Q, sigma, n, r, nullptr, st);
     pull_ctrl();
     r_host = r;
+    r_exact = r;
     check_status();
     initialized = true;
   }
@@ -916,7 +1091,7 @@ struct tsg_stream {
     ensure_partial(2 * 148 + 16);
     DecideArgs da;
     std::memset(&da, 0, sizeof da);
-    da.ctrl = ctrl;
+    da.slot = slots;
     da.nmodes = mode + 1;
     da.tau = tau;
     da.order = d;
@@ -925,14 +1100,14 @@ struct tsg_stream {
     da.cnt[mode] = project(yb, yd, mode, pb, partial);
     da.first_mode = mode;
     // decide() computes delta only for first_mode == 0; set it explicitly
-    ctrl_h->delta = delta;
-    ck(cudaMemcpyAsync(&ctrl->delta, &delta, 8, cudaMemcpyHostToDevice, st), "delta");
+    slots_h[0].delta = delta;
+    ck(cudaMemcpyAsync(&slots[0].delta, &slots_h[0].delta, 8, cudaMemcpyHostToDevice, st), "delta");
     launch_decide(da, st);
-    pull_ctrl();
-    const double res = std::sqrt(ctrl_h->res_sq[mode]);
+    pull_slot(0);
+    const double res = std::sqrt(slots_h[0].res_sq[mode]);
     const double* out = pb;
-    if (ctrl_h->expand_mode < 0) {
-      launch_commit_modes(ctrl, mode, mode + 1, 0, st);
+    if (slots_h[0].expand_mode < 0) {
+      launch_commit_modes(ctrl, slots, mode, mode + 1, 0, st);
       yd[mode] = R[mode];
     } else {
       // sized for yd[mode] <= N[mode]
@@ -1047,6 +1222,7 @@ void tsg_destroy(tsg_stream* h) {
   cudaSetDevice(h->device);
   if (h->st) cudaStreamSynchronize(h->st);
   h->free_all();
+  h->destroy_streams();
   if (h->st) cudaStreamDestroy(h->st);
   delete h;
 }

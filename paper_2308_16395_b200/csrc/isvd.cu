@@ -465,16 +465,16 @@ __device__ void pgram_block(const double* __restrict__ left, long long n_d, int 
   }
 }
 
-__device__ void finalize_record(Ctrl* c, double d, double cs, Metrics* rec, int order,
-                                const SpatialRanks& sr) {
+__device__ void finalize_record(Ctrl* c, const SliceCtl* sl, double d, double cs, Metrics* rec,
+                                int order, const SpatialRanks& sr) {
   // one batch of independent loads, then stores (no load-after-store chains)
   const int r_new = c->r_new, status = c->status, sweeps = c->sweeps;
   const long long n_d = c->n_d, ins = c->insertions;
-  const double slice_sq = c->slice_sq, proj_sq = c->proj_sq, margin = c->trunc_margin;
+  const double slice_sq = sl->slice_sq, proj_sq = c->proj_sq, margin = c->trunc_margin;
   const double sq_err = c->squared_error, ns = c->nonstream_discarded_sq, tot = c->total_input_sq;
   double res[kMaxD];
 #pragma unroll
-  for (int k = 0; k < kMaxD; ++k) res[k] = c->res_sq[k];
+  for (int k = 0; k < kMaxD; ++k) res[k] = sl->res_sq[k];
   c->coupling_diff_sq = d;
   c->core_sq = cs;
   if (sqrt(d) > kCouplingTol * sqrt(cs) + 1e-300 && status == 0) c->status = 2;  // streaming.cpp:55-63
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
     io.p = sp;
     io.k = sqrt(sh_esq);
     io.deg = (io.k <= kOrthEps * sqrt(sh_bsq)) ? 1 : 0;  // isvd.cpp:191
-    io.delta = c->delta;
+    io.delta = B.slot->delta;
     io.pgram = pg;
     io.inner = B.inner;
     io.sigma_new = B.sigma_new;
@@ -736,7 +736,7 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
   if (threadIdx.x == 0) {
     SpatialRanks sr;
     for (int k = 0; k < kMaxD; ++k) sr.v[k] = B.spatial_ranks[k];
-    finalize_record(c, dacc, cacc, B.metrics, B.order, sr);
+    finalize_record(c, B.slot, dacc, cacc, B.metrics, B.order, sr);
     TSG_CLK(9);
   }
 }
@@ -836,6 +836,7 @@ __global__ void __launch_bounds__(256) isvd_pass3_kernel(const Ctrl* ctrl, const
 
 struct InnerArgs {
   Ctrl* ctrl;
+  const SliceCtl* slot;
   const double* sigma;
   double* sigma_new;
   const double* part1;
@@ -883,7 +884,7 @@ __global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
   io.p = p;
   io.k = sqrt(sh_esq);
   io.deg = (io.k <= kOrthEps * sqrt(sh_bsq)) ? 1 : 0;
-  io.delta = c->delta;
+  io.delta = a.slot->delta;
   io.pgram = a.inner + L.pg;
   io.inner = a.inner;
   io.sigma_new = a.sigma_new;
@@ -939,8 +940,8 @@ __global__ void isvd_left_kernel(const Ctrl* ctrl, const double* __restrict__ le
             blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
-__global__ void isvd_finalize_kernel(Ctrl* c, const double* __restrict__ part, int nblk,
-                                     Metrics* rec, int order, SpatialRanks sr) {
+__global__ void isvd_finalize_kernel(Ctrl* c, const SliceCtl* sl, const double* __restrict__ part,
+                                     int nblk, Metrics* rec, int order, SpatialRanks sr) {
   __shared__ double red[32];
   double d = 0.0, cs = 0.0;
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
@@ -949,7 +950,7 @@ __global__ void isvd_finalize_kernel(Ctrl* c, const double* __restrict__ part, i
   }
   d = block_sum(d, red);
   cs = block_sum(cs, red);
-  if (threadIdx.x == 0) finalize_record(c, d, cs, rec, order, sr);
+  if (threadIdx.x == 0) finalize_record(c, sl, d, cs, rec, order, sr);
 }
 
 // ------------------------------------------------------- other entry points
@@ -1082,6 +1083,7 @@ void launch_isvd(const IsvdBufs& B, cudaStream_t st) {
                                                             part2, B.e, part3);
   InnerArgs ia;
   ia.ctrl = B.ctrl;
+  ia.slot = B.slot;
   ia.sigma = B.sigma;
   ia.sigma_new = B.sigma_new;
   ia.part1 = part1;
@@ -1112,7 +1114,7 @@ void launch_isvd(const IsvdBufs& B, cudaStream_t st) {
                                               capr, B.qn, B.cn, part4);
   isvd_left_kernel<<<grid_for((B.n_d + 1) * capr), 256, 0, st>>>(B.ctrl, B.left, B.n_d, capr,
                                                                   B.inner, B.left_new);
-  isvd_finalize_kernel<<<1, 256, 0, st>>>(B.ctrl, part4, gu, B.metrics, B.order, sr);
+  isvd_finalize_kernel<<<1, 256, 0, st>>>(B.ctrl, B.slot, part4, gu, B.metrics, B.order, sr);
   g_launches += 8;
 }
 

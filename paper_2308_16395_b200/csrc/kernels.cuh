@@ -73,6 +73,7 @@ struct ProjArgs {
   double* partial = nullptr;   // [grid * 2] (res_sq, x_sq) or nullptr
   int residual = 0;
   int stream_in = 0;           // input read once: evict-first loads
+  unsigned* tile_counter = nullptr;  // zeroed dynamic tile scheduler (optional)
 };
 // Returns the grid size (number of partial pairs written).
 int launch_project(const ProjArgs& a, cudaStream_t st);
@@ -83,7 +84,7 @@ void launch_sumsq(const double* x, long long n, double* out, double* scratch,
 
 // --------------------------------------------------------- streaming step
 struct DecideArgs {
-  Ctrl* ctrl;
+  SliceCtl* slot;
   const double* partial;     // concatenated partial pairs
   int off[kMaxD], cnt[kMaxD];
   int nmodes;                // d-1
@@ -94,7 +95,7 @@ struct DecideArgs {
 void launch_decide(const DecideArgs& a, cudaStream_t st);
 // Ledger commit for modes [m0, m1): nonstream += ||E_k||^2 as rn*rn;
 // with_total adds slice_norm^2 to total_input_sq (streaming.cpp:168-169).
-void launch_commit_modes(Ctrl* ctrl, int m0, int m1, int with_total,
+void launch_commit_modes(Ctrl* ctrl, const SliceCtl* slot, int m0, int m1, int with_total,
                          cudaStream_t st);
 void launch_ledger_add_nonstream(Ctrl* ctrl, const double* value, cudaStream_t st);
 
@@ -104,6 +105,7 @@ struct SpatialRanks {
 
 struct IsvdBufs {
   Ctrl* ctrl;
+  const SliceCtl* slot;  // this slice's decisions (delta, norms)
   const double* b;     // projected slice, length n
   const double* q;     // n x r (ld n)
   double* qn;          // n x r' out (ld n)

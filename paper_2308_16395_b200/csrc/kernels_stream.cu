@@ -126,7 +126,7 @@ __global__ void decide_kernel(DecideArgs a) {
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  Ctrl* c = a.ctrl;
+  SliceCtl* c = a.slot;
   if (a.first_mode == 0) {
     c->slice_sq = xsq;
     c->zero_slice = (xsq == 0.0);
@@ -141,14 +141,14 @@ __global__ void decide_kernel(DecideArgs a) {
   c->expand_mode = em;
 }
 
-__global__ void commit_modes_kernel(Ctrl* c, int m0, int m1, int with_total) {
+__global__ void commit_modes_kernel(Ctrl* c, const SliceCtl* s, int m0, int m1, int with_total) {
   if (threadIdx.x != 0) return;
   if (with_total) {
-    const double sn = sqrt(c->slice_sq);
+    const double sn = sqrt(s->slice_sq);
     c->total_input_sq += sn * sn;  // streaming.cpp:169
   }
   for (int k = m0; k < m1; ++k) {
-    const double rn = sqrt(c->res_sq[k]);
+    const double rn = sqrt(s->res_sq[k]);
     c->nonstream_discarded_sq += rn * rn;  // streaming.cpp:137
   }
 }
@@ -215,8 +215,9 @@ void launch_decide(const DecideArgs& a, cudaStream_t st) {
   ++g_launches;
 }
 
-void launch_commit_modes(Ctrl* ctrl, int m0, int m1, int with_total, cudaStream_t st) {
-  commit_modes_kernel<<<1, 32, 0, st>>>(ctrl, m0, m1, with_total);
+void launch_commit_modes(Ctrl* ctrl, const SliceCtl* slot, int m0, int m1, int with_total,
+                         cudaStream_t st) {
+  commit_modes_kernel<<<1, 32, 0, st>>>(ctrl, slot, m0, m1, with_total);
   ++g_launches;
 }
 

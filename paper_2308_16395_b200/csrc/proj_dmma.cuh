@@ -32,8 +32,12 @@ constexpr int red_doubles() {
   return 9 * MC * RT * 2 * 32;  // 8 warp partials + the reduced copy
 }
 
+// CTAs per SM for a tile shape: two when the register footprint allows, so
+// one CTA's reduction barriers overlap the other's DMMA work.
+constexpr int pick_minb(int RT, int MC, int GM) { return (MC * GM <= 8 && RT * MC <= 8) ? 2 : 1; }
+
 template <int RT, int MC, int GM>
-__global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int streaming_in) {
+__global__ void __launch_bounds__(256, pick_minb(RT, MC, GM)) proj_dmma_kernel(ProjArgs a, int streaming_in) {
   extern __shared__ double sm[];
   __shared__ double sred[32];
   constexpr int RPAD = 8 * RT + 4;
@@ -98,13 +102,30 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
     }
   };
 
+  // With one CTA per SM the next tile is prefetched into registers; with two,
+  // the co-resident CTA hides the load latency and registers stay <= 128.
+  constexpr bool kPrefetch = pick_minb(RT, MC, GM) == 1;
+  // Tiles are handed out by an atomic counter when one is given, so CTAs that
+  // start late (an SM busy with the previous slice's insertion) take fewer.
+  __shared__ long long s_next;
+  auto grab = [&]() -> long long {
+    if (a.tile_counter == nullptr) return -1;
+    __syncthreads();
+    if (threadIdx.x == 0) s_next = (long long)gridDim.x + atomicAdd(a.tile_counter, 1u);
+    __syncthreads();
+    return s_next;
+  };
   double racc = 0.0, xacc = 0.0;
   long long tile = blockIdx.x;
-  if (tile < ntiles) load_tile(tile, X);
+  long long next = a.tile_counter ? grab() : tile + gridDim.x;
+  if (kPrefetch && tile < ntiles) load_tile(tile, X);
 #pragma unroll 1
-  for (; tile < ntiles; tile += gridDim.x) {
-    const long long next = tile + gridDim.x;
-    if (next < ntiles) load_tile(next, Xn);
+  for (; tile < ntiles;) {
+    if (kPrefetch) {
+      if (next < ntiles) load_tile(next, Xn);
+    } else {
+      load_tile(tile, X);
+    }
     // ---- phase 1: partial P^T over the warp's rows
     double acc[MC][RT][2];
 #pragma unroll
@@ -216,13 +237,17 @@ __global__ void __launch_bounds__(256, 1) proj_dmma_kernel(ProjArgs a, int strea
         }
       }
     }
+    if (kPrefetch) {
 #pragma unroll
-    for (int mc = 0; mc < MC; ++mc)
+      for (int mc = 0; mc < MC; ++mc)
 #pragma unroll
-      for (int gi = 0; gi < GM; ++gi) {
-        X[mc][gi][0] = Xn[mc][gi][0];
-        X[mc][gi][1] = Xn[mc][gi][1];
-      }
+        for (int gi = 0; gi < GM; ++gi) {
+          X[mc][gi][0] = Xn[mc][gi][0];
+          X[mc][gi][1] = Xn[mc][gi][1];
+        }
+    }
+    tile = next;
+    next = a.tile_counter ? grab() : tile + gridDim.x;
   }
   racc = block_sum(racc, sred);
   xacc = block_sum(xacc, sred);
@@ -250,14 +275,16 @@ inline int launch_t(const ProjArgs& a, int streaming_in, cudaStream_t st) {
   }
   const long long cols = a.v.left * a.v.right;
   const long long ntiles = (cols + 8 * MC - 1) / (8 * MC);
-  const int grid = (int)(ntiles < kNumSMs ? (ntiles < 1 ? 1 : ntiles) : kNumSMs);
+  // one SM is left to the concurrently running insertion kernel
+  const long long slots = (long long)(kNumSMs - 1) * pick_minb(RT, MC, GM);
+  const int grid = (int)(ntiles < slots ? (ntiles < 1 ? 1 : ntiles) : slots);
   proj_dmma_kernel<RT, MC, GM><<<grid, 256, smem, st>>>(a, streaming_in);
   return grid;
 }
 
 // Column tiles per CTA tile: wide tiles for small R (B-fragment reuse), while
 // keeping the register-resident X (2 MC GM doubles, double-buffered) bounded.
-constexpr int pick_mc(int RT, int GM) { return RT <= 2 ? (GM <= 4 ? 4 : 2) : (RT <= 6 ? 2 : 1); }
+constexpr int pick_mc(int RT, int GM) { return RT <= 2 ? (GM <= 2 ? 4 : 2) : (RT <= 6 ? 2 : 1); }
 
 template <int RT, int GM>
 inline int launch_rt(const ProjArgs& a, int streaming_in, cudaStream_t st) {
