@@ -621,18 +621,23 @@ struct tsg_stream {
                                   std::chrono::steady_clock::now() - t0).count()});
   }
 
-  void update(const double* y_in, int mem_kind) {
-    const auto t0 = std::chrono::steady_clock::now();
-    if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
-    const int par = (int)(upd_count++ & 1);
-    const double* y = y_in;
-    if (mem_kind == TSG_MEM_HOST) {
-      ck(cudaMemcpyAsync(slice, y_in, sizeof(double) * slice_elems, cudaMemcpyHostToDevice, st),
-         "slice H2D");
-      y = slice;
-    }
+  // A slice whose projections are enqueued but whose decision (basis growth,
+  // zero slice) has not been acted on yet.
+  struct Pend {
+    int par = 0;
+    const double* y = nullptr;  // device input (caller buffer or staging)
+    const double* b = nullptr;  // projected tensor
+    std::chrono::steady_clock::time_point t0;
+    std::array<cudaEvent_t, 3> ev{};
+  };
+  Pend prev;
+  bool have_prev = false;
+  double* stage[2] = {nullptr, nullptr};  // host-slice staging per parity
+
+  void enqueue_proj(const double* y, Pend& p) {
+    const int par = p.par;
     ensure_pipe();
-    // this parity's buffers were last read by the insertion two slices ago
+    // this parity's buffers and slot were last read by the insertion two slices ago
     if (ev_isvd_valid[par]) ck(cudaStreamWaitEvent(st, ev_isvd[par], 0), "cudaStreamWaitEvent");
     long long yd[kMaxD];
     for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
@@ -658,19 +663,56 @@ struct tsg_stream {
     da.first_mode = 0;
     launch_decide(da, st);
     ev_mark(2, st);
+    p.ev = {ev_cur[0], ev_cur[1], ev_cur[2]};
     ck(cudaMemcpyAsync(slots_h + par, slots + par, sizeof(SliceCtl), cudaMemcpyDeviceToHost, st),
        "slot D2H");
     ck(cudaEventRecord(ev_proj[par], st), "cudaEventRecord");
-    // the previous slice's insertion keeps running on si meanwhile
-    ck(cudaEventSynchronize(ev_proj[par]), "cudaEventSynchronize");
+    p.y = y;
+    p.b = cur;
+  }
+
+  // Act on a slice's decision. Returns true when the slow path ran (the
+  // non-streaming bases may have grown, so later projections must be redone).
+  bool complete(Pend& p) {
+    ck(cudaEventSynchronize(ev_proj[p.par]), "cudaEventSynchronize");
     ck(cudaGetLastError(), "kernel");
-    const SliceCtl& sc = slots_h[par];
+    const SliceCtl& sc = slots_h[p.par];
     if (sc.zero_slice || sc.expand_mode >= 0) {
-      update_slow(y, par, t0);
-    } else {
-      enqueue_isvd(cur, par, 0, si, true, t0);
+      update_slow(p.y, p.par, p.t0);
+      return true;
     }
-    if (!(flags & TSG_ASYNC)) {
+    ev_cur[0] = p.ev[0];
+    ev_cur[1] = p.ev[1];
+    ev_cur[2] = p.ev[2];
+    enqueue_isvd(p.b, p.par, 0, si, true, p.t0);
+    return false;
+  }
+
+  void update(const double* y_in, int mem_kind) {
+    if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
+    Pend cur;
+    cur.t0 = std::chrono::steady_clock::now();
+    cur.par = (int)(upd_count++ & 1);
+    const double* y = y_in;
+    if (mem_kind == TSG_MEM_HOST) {
+      if (!stage[cur.par]) stage[cur.par] = dalloc(slice_elems);
+      ck(cudaMemcpyAsync(stage[cur.par], y_in, sizeof(double) * slice_elems,
+                         cudaMemcpyHostToDevice, st), "slice H2D");
+      y = stage[cur.par];
+    }
+    // enqueue this slice first, then settle the previous one: the projection
+    // stream never waits on the host
+    enqueue_proj(y, cur);
+    if (have_prev) {
+      have_prev = false;
+      if (complete(prev)) enqueue_proj(y, cur);  // bases grew: redo this slice
+    }
+    if (flags & TSG_ASYNC) {
+      prev = cur;
+      have_prev = true;
+      drain(false);
+    } else {
+      complete(cur);
       drain(true);
       pull_ctrl();
       check_status();
@@ -772,6 +814,10 @@ struct tsg_stream {
   }
 
   void flush() {
+    if (have_prev) {
+      have_prev = false;
+      complete(prev);
+    }
     sync();
     drain(true);
     pull_ctrl();
@@ -927,6 +973,8 @@ struct tsg_stream {
     core = core2 = Q = Q2 = sigma = sigma2 = left = left2 = nullptr;
     slice = slice_b = w0 = w1 = w2 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
     tile_ctr = nullptr;
+    stage[0] = stage[1] = nullptr;
+    have_prev = false;
     partial_cap = ipart_cap = 0;
     evec_n = 0;
     metrics.clear();
