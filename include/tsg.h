@@ -32,9 +32,11 @@
  * the streaming factor ("left") exported column-major n_d x r as
  * StreamingState::streaming_factor() returns it.
  *
- * Memory: TSG_MEM_HOST pointers are copied to the device inside the call;
- * TSG_MEM_DEVICE pointers must be device-resident fp64 buffers that stay
- * valid until the call returns (or until tsg_synchronize in async mode).
+ * Memory: TSG_MEM_HOST slices are copied to device staging on a copy
+ * stream; TSG_MEM_DEVICE pointers must be device-resident fp64 buffers. In
+ * the default synchronous mode a slice may be reused as soon as tsg_update
+ * returns. With TSG_ASYNC, a slice (host or device) must stay unchanged
+ * until the following tsg_update (or tsg_synchronize) returns.
  * The handle owns all device memory; one host thread drives a handle.
  */
 #ifndef TSG_H
@@ -124,6 +126,9 @@ int64_t tsg_metrics_count(tsg_stream* h);
 int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out);
 int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out);
 
+/* Bytes the engine reads back per absorbed slice (decision slot, control
+ * block snapshot, metrics record). */
+int64_t tsg_readback_bytes_per_update(void);
 /* Number of kernels this handle has launched (for launch accounting). */
 int64_t tsg_kernel_launches(tsg_stream* h);
 /* The CUDA stream the handle enqueues on (cudaStream_t as void*). */

@@ -90,12 +90,17 @@ struct tsg_stream {
   double* pgram = nullptr;
   double* inner = nullptr;
   unsigned* tile_ctr = nullptr;  // dynamic tile-scheduler counters
+  double* upad[kMaxD] = {nullptr};  // pre-padded U_k images (proj_dmma smem layout)
+  long long upad_R[kMaxD] = {0};    // rank the image was built for
   unsigned ctr_next = 0;
   Ctrl* ctrl = nullptr;
   Ctrl* ctrl_h = nullptr;
   // two-stage pipeline: projections of slice t+1 (stream st) overlap the
   // ISVD of slice t (stream si); per-parity decision slots and work buffers
   cudaStream_t si = nullptr;
+  cudaStream_t sc = nullptr;     // host-to-device copies (overlap with compute)
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
+  bool ev_h2d_valid[2] = {false, false};
   SliceCtl* slots = nullptr;     // device [2]
   SliceCtl* slots_h = nullptr;   // pinned mirror [2]
   double* pw[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
@@ -189,6 +194,7 @@ struct tsg_stream {
   void free_all() {
     if (st) cudaStreamSynchronize(st);
     if (si) cudaStreamSynchronize(si);
+    if (sc) cudaStreamSynchronize(sc);
     for (auto& a : allocs) cudaFree(a.first);
     allocs.clear();
     cur_bytes = 0;
@@ -202,8 +208,9 @@ struct tsg_stream {
     slots_h = nullptr;
   }
 
-  // both streams
+  // all streams
   void sync() {
+    if (sc) ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
     ck(cudaStreamSynchronize(si), "cudaStreamSynchronize");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   }
@@ -436,6 +443,13 @@ struct tsg_stream {
     a.partial = part;
     a.residual = 1;
     a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? 1 : 0;
+    if (upad_R[mode] != R[mode]) {
+      dfree(upad[mode]);
+      upad[mode] = dalloc(upad_size(N[mode], (int)R[mode]));
+      launch_pad_u(U[mode], N[mode], (int)R[mode], upad[mode], st);
+      upad_R[mode] = R[mode];
+    }
+    a.upad = upad[mode];
     if (!tile_ctr) tile_ctr = reinterpret_cast<unsigned*>(dalloc(kMaxD * 2));
     a.tile_counter = tile_ctr + (ctr_next++ % (kMaxD * 4));
     ck(cudaMemsetAsync(a.tile_counter, 0, sizeof(unsigned), st), "memset");
@@ -695,10 +709,18 @@ struct tsg_stream {
     cur.par = (int)(upd_count++ & 1);
     const double* y = y_in;
     if (mem_kind == TSG_MEM_HOST) {
+      // copy engine stream: the H2D of slice t overlaps compute of slice t-1;
+      // staging[par] is free once the projections that read it are done
       if (!stage[cur.par]) stage[cur.par] = dalloc(slice_elems);
+      ck(cudaStreamWaitEvent(sc, ev_proj[cur.par], 0), "cudaStreamWaitEvent");
       ck(cudaMemcpyAsync(stage[cur.par], y_in, sizeof(double) * slice_elems,
-                         cudaMemcpyHostToDevice, st), "slice H2D");
+                         cudaMemcpyHostToDevice, sc), "slice H2D");
+      ck(cudaEventRecord(ev_h2d[cur.par], sc), "cudaEventRecord");
+      ev_h2d_valid[cur.par] = true;
+      ck(cudaStreamWaitEvent(st, ev_h2d[cur.par], 0), "cudaStreamWaitEvent");
       y = stage[cur.par];
+      // the caller's previous host slice has been consumed once its copy ends
+      if (ev_h2d_valid[cur.par ^ 1]) ck(cudaEventSynchronize(ev_h2d[cur.par ^ 1]), "h2d sync");
     }
     // enqueue this slice first, then settle the previous one: the projection
     // stream never waits on the host
@@ -973,6 +995,10 @@ struct tsg_stream {
     core = core2 = Q = Q2 = sigma = sigma2 = left = left2 = nullptr;
     slice = slice_b = w0 = w1 = w2 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
     tile_ctr = nullptr;
+    for (int k = 0; k < kMaxD; ++k) {
+      upad[k] = nullptr;
+      upad_R[k] = 0;
+    }
     stage[0] = stage[1] = nullptr;
     have_prev = false;
     partial_cap = ipart_cap = 0;
@@ -991,6 +1017,11 @@ struct tsg_stream {
     n_d = 0;
     insertions_host = 0;
     if (!si) ck(cudaStreamCreateWithFlags(&si, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!sc) ck(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i) {
+      if (!ev_h2d[i]) ck(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming), "event");
+      ev_h2d_valid[i] = false;
+    }
     for (int i = 0; i < 2; ++i) {
       if (!ev_proj[i]) ck(cudaEventCreateWithFlags(&ev_proj[i], cudaEventDisableTiming), "event");
       if (!ev_isvd[i]) ck(cudaEventCreateWithFlags(&ev_isvd[i], cudaEventDisableTiming), "event");
@@ -1017,8 +1048,12 @@ struct tsg_stream {
     for (auto& e : ev_rec)
       if (e) cudaEventDestroy(e);
     for (auto e : ev_pool) cudaEventDestroy(e);
+    for (int i = 0; i < 2; ++i)
+      if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
     if (si) cudaStreamDestroy(si);
+    if (sc) cudaStreamDestroy(sc);
     si = nullptr;
+    sc = nullptr;
   }
 
   // ------------------------------------------------------ export/import
@@ -1383,6 +1418,10 @@ int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tfl
 }
 
 int tsg_debug_isvd_clocks(int64_t* out) { return tsg::read_isvd_clocks(reinterpret_cast<long long*>(out)); }
+
+int64_t tsg_readback_bytes_per_update(void) {
+  return (int64_t)(sizeof(Ctrl) + sizeof(Metrics) + sizeof(SliceCtl));
+}
 
 int64_t tsg_kernel_launches(tsg_stream* h) { return h ? g_launches - h->launches_at_create : g_launches; }
 

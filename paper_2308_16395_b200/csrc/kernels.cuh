@@ -74,7 +74,13 @@ struct ProjArgs {
   int residual = 0;
   int stream_in = 0;           // input read once: evict-first loads
   unsigned* tile_counter = nullptr;  // zeroed dynamic tile scheduler (optional)
+  const double* upad = nullptr;      // optional pre-padded U image (see pad_u)
 };
+// Pre-padded U image for the DMMA projection kernel: rows padded to a
+// multiple of 8, row pitch 8*ceil(R/8)+4, zero fill. Returns its size in
+// doubles for (N, R); writes it when `out` is non-null.
+long long upad_size(long long N, int R);
+void launch_pad_u(const double* u, long long N, int R, double* out, cudaStream_t st);
 // Returns the grid size (number of partial pairs written).
 int launch_project(const ProjArgs& a, cudaStream_t st);
 

@@ -157,7 +157,31 @@ __global__ void ledger_add_kernel(Ctrl* c, const double* v) {
   if (threadIdx.x == 0) c->nonstream_discarded_sq += *v;  // streaming.cpp:150
 }
 
+__global__ void pad_u_kernel(const double* __restrict__ u, long long N, int R, int rpad,
+                             long long rows8, double* __restrict__ out) {
+  const long long total = rows8 * rpad;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long row = idx / rpad;
+    const int col = (int)(idx % rpad);
+    out[idx] = (row < N && col < R) ? u[row + col * N] : 0.0;
+  }
+}
+
 }  // namespace
+
+long long upad_size(long long N, int R) {
+  const long long rows8 = (N + 7) / 8 * 8;
+  const int rpad = 8 * ((R + 7) / 8) + 4;
+  return rows8 * rpad;
+}
+
+void launch_pad_u(const double* u, long long N, int R, double* out, cudaStream_t st) {
+  const long long rows8 = (N + 7) / 8 * 8;
+  const int rpad = 8 * ((R + 7) / 8) + 4;
+  pad_u_kernel<<<(int)((rows8 * rpad + 255) / 256), 256, 0, st>>>(u, N, R, rpad, rows8, out);
+  ++g_launches;
+}
 
 namespace {
 

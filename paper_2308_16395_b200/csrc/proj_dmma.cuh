@@ -48,7 +48,14 @@ __global__ void __launch_bounds__(256, pick_minb(RT, MC, GM)) proj_dmma_kernel(P
   const int ngroups = (int)((N + 7) / 8);
   double* Us = sm;
   double* red = Us + (long long)ngroups * 8 * RPAD;
-  {
+  if (a.upad) {
+    // straight 16-byte copy of the pre-padded image (RPAD is even)
+    const int total2 = ngroups * 8 * RPAD / 2;
+    const double2* src = reinterpret_cast<const double2*>(a.upad);
+    double2* dst = reinterpret_cast<double2*>(Us);
+#pragma unroll 8
+    for (int idx = threadIdx.x; idx < total2; idx += blockDim.x) dst[idx] = __ldg(src + idx);
+  } else {
     // coalesced read of the column-major U, transposed into the padded rows
     const int rows8 = ngroups * 8;
     const int total = rows8 * RPAD;
@@ -107,17 +114,21 @@ __global__ void __launch_bounds__(256, pick_minb(RT, MC, GM)) proj_dmma_kernel(P
   constexpr bool kPrefetch = pick_minb(RT, MC, GM) == 1;
   // Tiles are handed out by an atomic counter when one is given, so CTAs that
   // start late (an SM busy with the previous slice's insertion) take fewer.
+  // The index two tiles ahead is fetched by thread 0 at the start of a tile
+  // and published at the reduction barrier, so the atomic's latency hides
+  // behind phase 1.
   __shared__ long long s_next;
-  auto grab = [&]() -> long long {
-    if (a.tile_counter == nullptr) return -1;
-    __syncthreads();
-    if (threadIdx.x == 0) s_next = (long long)gridDim.x + atomicAdd(a.tile_counter, 1u);
-    __syncthreads();
-    return s_next;
-  };
+  const bool dyn = a.tile_counter != nullptr;
   double racc = 0.0, xacc = 0.0;
   long long tile = blockIdx.x;
-  long long next = a.tile_counter ? grab() : tile + gridDim.x;
+  long long next;
+  if (dyn) {
+    if (threadIdx.x == 0) s_next = (long long)gridDim.x + atomicAdd(a.tile_counter, 1u);
+    __syncthreads();
+    next = s_next;
+  } else {
+    next = tile + gridDim.x;
+  }
   if (kPrefetch && tile < ntiles) load_tile(tile, X);
 #pragma unroll 1
   for (; tile < ntiles;) {
@@ -126,6 +137,8 @@ __global__ void __launch_bounds__(256, pick_minb(RT, MC, GM)) proj_dmma_kernel(P
     } else {
       load_tile(tile, X);
     }
+    long long after = 0;
+    if (dyn && threadIdx.x == 0) after = (long long)gridDim.x + atomicAdd(a.tile_counter, 1u);
     // ---- phase 1: partial P^T over the warp's rows
     double acc[MC][RT][2];
 #pragma unroll
@@ -157,6 +170,7 @@ __global__ void __launch_bounds__(256, pick_minb(RT, MC, GM)) proj_dmma_kernel(P
       for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
         for (int i = 0; i < 2; ++i) myred[((mc * RT + rt) * 2 + i) * 32 + lane] = acc[mc][rt][i];
+    if (dyn && threadIdx.x == 0) s_next = after;
     __syncthreads();
     double* fin = red + 8 * (PER * 32);
     for (int slot = warp; slot < PER; slot += 8) {
@@ -247,7 +261,7 @@ __global__ void __launch_bounds__(256, pick_minb(RT, MC, GM)) proj_dmma_kernel(P
         }
     }
     tile = next;
-    next = a.tile_counter ? grab() : tile + gridDim.x;
+    next = dyn ? s_next : tile + gridDim.x;
   }
   racc = block_sum(racc, sred);
   xacc = block_sum(xacc, sred);

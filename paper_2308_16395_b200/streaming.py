@@ -93,7 +93,7 @@ EXPORTED = [
     "tsg_estimate_relative_error", "tsg_metrics_count", "tsg_metrics_at", "tsg_last_metrics",
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
-    "tsg_measure_fp64_peaks",
+    "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update",
 ]
 
 _LIB = None
@@ -141,6 +141,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                           _dp]
     L.tsg_profile.argtypes = [C.c_void_p, _dp, C.c_int32, C.c_int32]
     L.tsg_measure_fp64_peaks.argtypes = [C.c_int32, _dp, _dp]
+    L.tsg_readback_bytes_per_update.argtypes = []
+    L.tsg_readback_bytes_per_update.restype = C.c_int64
     _LIB = L
     return L
 
@@ -394,6 +396,10 @@ def assemble_streaming_state(st: State, device: int = 0, asynchronous: bool = Fa
     out._check(out.L.tsg_import_state(out.h, C.byref(dm), _p(core), _p(fac), _p(sig), _p(left),
                                       _p(right)))
     return out
+
+
+def readback_bytes_per_update() -> int:
+    return int(load_library().tsg_readback_bytes_per_update())
 
 
 def measure_fp64_peaks(device: int = 0) -> tuple[float, float]:
