@@ -7,6 +7,8 @@ namespace tsg {
 
 constexpr int kMaxD = 8;
 constexpr int kNumSMs = 148;
+// Upper bound on the CTAs of any partial-sum-producing kernel (2 per SM).
+constexpr int kMaxGrid = 2 * kNumSMs;
 
 // Numeric constants that parity depends on (SURVEY §5 "Config / flags").
 constexpr double kCouplingTol = 1e-8;       // streaming.cpp:15

@@ -246,7 +246,7 @@ struct tsg_stream {
   // Partials for every mode plus one spare region, allocated once so that
   // pointers captured by enqueued kernels stay valid.
   void ensure_partial(long long n) {
-    const long long need = std::max(n, 2LL * 148 * (kMaxD + 1) + 64);
+    const long long need = std::max(n, 2LL * kMaxGrid * (kMaxD + 1) + 64);
     if (need <= partial_cap) return;
     if (partial) sync();
     dfree(partial);
@@ -465,7 +465,7 @@ struct tsg_stream {
     if (!kbuf) kbuf = dalloc(slice_elems);
     ModeView v{prod(yd, mode), yd[mode], prod(yd + mode + 1, d - 2 - mode)};
     dbg("expand: entry");
-    project(y, yd, mode, p, partial + 2LL * 148 * kMaxD, ebuf);
+    project(y, yd, mode, p, partial + 2LL * kMaxGrid * kMaxD, ebuf);
     dbg("expand: residual");
     Sub s = mode_subspace(ebuf, yd, d - 1, mode, delta);
     dbg("expand: mode_subspace");
@@ -790,7 +790,7 @@ struct tsg_stream {
       const double* cur = base;
       for (int k = m0; k < em; ++k) {
         double* out = pick(cur, base);
-        project(cur, yd, k, out, partial + 2LL * 148 * kMaxD);
+        project(cur, yd, k, out, partial + 2LL * kMaxGrid * kMaxD);
         yd[k] = R[k];
         cur = out;
       }

@@ -163,3 +163,50 @@ def test_config2_full_size_vs_oracle(oracle):
     sc = P.compare_states(sg, so)
     print("c2", mc, sc)
     P.assert_parity(mc, sc)
+
+
+def _oracle_run(oracle, case):
+    x = case.init_flat.reshape(case.init_dims[::-1]).transpose()
+    h = oracle.stream_init(x, case.tau)
+    for s in case.slices:
+        h.update_flat(s)
+    return h
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("size,every", [(64, 12), (96, 15)])
+def test_growth_midsize_vs_oracle(oracle, size, every):
+    """Config-5 generator (rank growth) at sizes where the projection grid is
+    full (>= 2 CTAs per SM) and expansions run the large Gram/Jacobi path."""
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.scaled(dg.CONFIGS["c5"], (size,) * 3, n_slices=10 + 3 * every + 2, n_init=10,
+                    name=f"growth{size}")
+    cfg.growth = (6, 3, every, 12)
+    cfg.spatial_ranks = (12, 12, 12)
+    cfg.time_rank = 12
+    case = cases.config_case(cfg)
+    st = run_gpu(case, asynchronous=True)
+    ho = _oracle_run(oracle, case)
+    sg, so = st.export(), ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(st.metrics(), sg.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(sg, so)
+    print(size, mc, sc)
+    assert int(np.count_nonzero(P.metrics_arrays(ho.metrics(), so.order)["expanded_mask"])) >= 2
+    P.assert_parity(mc, sc)
+
+
+@pytest.mark.slow
+def test_config3_generator_midsize_vs_oracle(oracle):
+    """Config-3 generator (geometric core spectrum, R = 32) at 96^3."""
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.scaled(dg.CONFIGS["c3"], (96, 96, 96), n_slices=14, n_init=5, name="c3_96")
+    case = cases.config_case(cfg)
+    st = run_gpu(case, asynchronous=True)
+    ho = _oracle_run(oracle, case)
+    sg, so = st.export(), ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(st.metrics(), sg.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(sg, so)
+    print("c3_96", mc, sc)
+    P.assert_parity(mc, sc)
