@@ -10,6 +10,7 @@
 //   orthonormalize_columns src/linalg.cpp:64-78
 //   orthonormality_defect src/matrix.cpp:118-131
 //   unfold / pad / concat src/tensor.cpp:67-84, 168-209
+#include <algorithm>
 #include <cfloat>
 
 #include "kernels.cuh"
@@ -494,9 +495,14 @@ inline int grid_for(long long total, int block = 256, int cap = 148 * 16) {
 
 }  // namespace
 
+bool launch_sym_eig_coop(const double* g, int n, double* evals, double* evecs, double* work,
+                         double* part, int* sweeps_out, cudaStream_t st);
+
 void launch_sym_eig(const double* g, int n, double* evals, double* evecs, double* work,
                     int* sweeps_out, cudaStream_t st) {
   if (n <= 0) return;
+  // work holds 2 n^2 doubles plus room for per-CTA partials (see engine)
+  if (launch_sym_eig_coop(g, n, evals, evecs, work, work + 2LL * n * n, sweeps_out, st)) return;
   const size_t smem = sizeof(Rot) * ((n + 2) / 2) + sizeof(int) * (n + 1);
   static bool attr = false;
   if (!attr) {
@@ -589,6 +595,232 @@ void launch_sumsq(const double* x, long long n, double* out, double* scratch, cu
   sumsq_partial_kernel<<<g, 256, 0, st>>>(x, n, scratch);
   sum_kernel<<<1, 1024, 0, st>>>(scratch, g, out);
   g_launches += 2;
+}
+
+}  // namespace tsg
+
+// ---------------------------------------------------------------------------
+// Cooperative multi-CTA Jacobi for large symmetric matrices (basis growth and
+// stream_init Gram matrices, n up to a few hundred). Same ordering, formulas,
+// stopping rule and finishing steps as the single-CTA solver; every CTA
+// recomputes the round's rotations from the (grid-synchronised) matrix and
+// applies its share of the 2x2 block and V updates, with one grid barrier
+// per round.
+#include <cooperative_groups.h>
+
+namespace tsg {
+namespace {
+
+namespace cg = cooperative_groups;
+
+struct RotC {
+  double c, s, t;
+  int p, q;
+};
+
+__global__ void __launch_bounds__(256) sym_eig_coop_kernel(const double* __restrict__ gin, int n,
+                                                           double* evals, double* evecs,
+                                                           double* work, double* part,
+                                                           int* sweeps_out) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ unsigned char smem_raw[];
+  RotC* rot = reinterpret_cast<RotC*>(smem_raw);
+  __shared__ double red[32];
+  double* G = work;
+  double* V = work + (long long)n * n;
+  const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  const long long gstride = (long long)gridDim.x * blockDim.x;
+  const long long nn = (long long)n * n;
+  double acc = 0.0;
+  for (long long idx = gtid; idx < nn; idx += gstride) {
+    const double g = gin[idx];
+    G[idx] = g;
+    V[idx] = ((idx % n) == (idx / n)) ? 1.0 : 0.0;
+    acc += g * g;
+  }
+  acc = block_sum(acc, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = acc;
+  grid.sync();
+  double tot = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) tot += part[b];
+  const double tol = kOffDiagTolFactor * sqrt(tot);
+  const int np = n + (n & 1), half = np / 2;
+  int sweep = 0;
+  for (; sweep < kMaxSweeps; ++sweep) {
+    double o2 = 0.0;
+    for (long long idx = gtid; idx < nn; idx += gstride) {
+      const int i = (int)(idx % n), j = (int)(idx / n);
+      if (i != j) o2 += G[idx] * G[idx];
+    }
+    o2 = block_sum(o2, red);
+    grid.sync();  // everyone has read G before partials are overwritten
+    if (threadIdx.x == 0) part[blockIdx.x] = o2;
+    grid.sync();
+    double off = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) off += part[b];
+    off = sqrt(off);
+    if (off <= tol || n < 2) break;
+    for (int rd = 0; rd < np - 1; ++rd) {
+      for (int m = threadIdx.x; m < half; m += blockDim.x) {
+        int a, b;
+        if (m == 0) {
+          a = rd % (np - 1);
+          b = np - 1;
+        } else {
+          a = (rd + m) % (np - 1);
+          b = (rd + np - 1 - m) % (np - 1);
+        }
+        RotC R;
+        R.p = min(a, b);
+        R.q = max(a, b);
+        R.c = 1.0;
+        R.s = 0.0;
+        R.t = 0.0;
+        if (R.q < n) {
+          const double gpq = G[R.p + (long long)R.q * n];
+          if (gpq != 0.0) {
+            const double gpp = G[R.p + (long long)R.p * n];
+            const double gqq = G[R.q + (long long)R.q * n];
+            const double theta = (gqq - gpp) / (2.0 * gpq);
+            const double t = (theta >= 0.0) ? 1.0 / (theta + sqrt(1.0 + theta * theta))
+                                            : 1.0 / (theta - sqrt(1.0 + theta * theta));
+            const double c = 1.0 / sqrt(1.0 + t * t);
+            R.c = c;
+            R.s = t * c;
+            R.t = t;
+          }
+        }
+        rot[m] = R;
+      }
+      // every CTA has read the pairs' entries before any diagonal block moves
+      grid.sync();
+      const long long nblk = (long long)half * half;
+      for (long long bi = gtid; bi < nblk; bi += gstride) {
+        const int m1 = (int)(bi / half), m2 = (int)(bi % half);
+        if (m1 > m2) continue;
+        const RotC A = rot[m1], B = rot[m2];
+        const bool idA = (A.s == 0.0 && A.t == 0.0), idB = (B.s == 0.0 && B.t == 0.0);
+        if (idA && idB) continue;
+        const int p1 = A.p, q1 = A.q, p2 = B.p, q2 = B.q;
+        const bool q1v = q1 < n, q2v = q2 < n;
+        if (m1 == m2) {
+          const double gpq = G[p1 + (long long)q1 * n];
+          const double gpp = G[p1 + (long long)p1 * n];
+          const double gqq = G[q1 + (long long)q1 * n];
+          G[p1 + (long long)p1 * n] = gpp - A.t * gpq;
+          G[q1 + (long long)q1 * n] = gqq + A.t * gpq;
+          G[p1 + (long long)q1 * n] = 0.0;
+          G[q1 + (long long)p1 * n] = 0.0;
+          continue;
+        }
+        const double b00 = G[p1 + (long long)p2 * n];
+        const double b01 = q2v ? G[p1 + (long long)q2 * n] : 0.0;
+        const double b10 = q1v ? G[q1 + (long long)p2 * n] : 0.0;
+        const double b11 = (q1v && q2v) ? G[q1 + (long long)q2 * n] : 0.0;
+        const double t00 = A.c * b00 - A.s * b10, t01 = A.c * b01 - A.s * b11;
+        const double t10 = A.s * b00 + A.c * b10, t11 = A.s * b01 + A.c * b11;
+        const double o00 = B.c * t00 - B.s * t01, o01 = B.s * t00 + B.c * t01;
+        const double o10 = B.c * t10 - B.s * t11, o11 = B.s * t10 + B.c * t11;
+        G[p1 + (long long)p2 * n] = o00;
+        G[p2 + (long long)p1 * n] = o00;
+        if (q2v) {
+          G[p1 + (long long)q2 * n] = o01;
+          G[q2 + (long long)p1 * n] = o01;
+        }
+        if (q1v) {
+          G[q1 + (long long)p2 * n] = o10;
+          G[p2 + (long long)q1 * n] = o10;
+        }
+        if (q1v && q2v) {
+          G[q1 + (long long)q2 * n] = o11;
+          G[q2 + (long long)q1 * n] = o11;
+        }
+      }
+      for (long long idx = gtid; idx < (long long)n * half; idx += gstride) {
+        const int i = (int)(idx % n), m = (int)(idx / n);
+        const RotC R = rot[m];
+        if (R.q >= n || (R.s == 0.0 && R.t == 0.0)) continue;
+        const double vp = V[i + (long long)R.p * n], vq = V[i + (long long)R.q * n];
+        V[i + (long long)R.p * n] = R.c * vp - R.s * vq;
+        V[i + (long long)R.q * n] = R.s * vp + R.c * vq;
+      }
+      grid.sync();
+    }
+  }
+  if (blockIdx.x != 0) return;
+  // finish (stable sort, clamp, sign rule) in CTA 0
+  int* perm = reinterpret_cast<int*>(rot);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double di = G[i + (long long)i * n];
+    int rank = 0;
+    for (int j = 0; j < n; ++j) {
+      const double dj = G[j + (long long)j * n];
+      if (dj > di || (dj == di && j < i)) ++rank;
+    }
+    perm[rank] = i;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < n; j += nw) {
+    const int src = perm[j];
+    double lambda = G[src + (long long)src * n];
+    if (lambda < 0.0) lambda = 0.0;
+    if (lane == 0) evals[j] = lambda;
+    double best = -1.0;
+    int arg = 0x7fffffff;
+    for (int i = lane; i < n; i += 32) {
+      const double a = fabs(V[i + (long long)src * n]);
+      if (a > best) {
+        best = a;
+        arg = i;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oa = __shfl_xor_sync(0xffffffffu, arg, o);
+      if (ob > best || (ob == best && oa < arg)) {
+        best = ob;
+        arg = oa;
+      }
+    }
+    const bool flip = V[arg + (long long)src * n] < 0.0;
+    for (int i = lane; i < n; i += 32) {
+      const double v = V[i + (long long)src * n];
+      evecs[i + (long long)j * n] = flip ? -v : v;
+    }
+  }
+  if (threadIdx.x == 0 && sweeps_out) *sweeps_out = sweep;
+}
+
+}  // namespace
+
+// Large n: cooperative grid (one CTA per SM at most); small n: one CTA.
+bool launch_sym_eig_coop(const double* g, int n, double* evals, double* evecs, double* work,
+                         double* part, int* sweeps_out, cudaStream_t st) {
+  if (n < 96) return false;
+  int dev = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return false;
+  const size_t smem = std::max(sizeof(RotC) * ((n + 2) / 2), sizeof(int) * (n + 1));
+  cudaFuncSetAttribute(sym_eig_coop_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sym_eig_coop_kernel, 256, smem);
+  int sms = kNumSMs;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  long long want = ((long long)n * n / 4 + 255) / 256;
+  int grid = (int)std::min<long long>(std::max<long long>(want, 1), (long long)sms * std::max(per_sm, 1));
+  grid = std::min(grid, 256);
+  void* args[] = {(void*)&g, (void*)&n, (void*)&evals, (void*)&evecs, (void*)&work, (void*)&part,
+                  (void*)&sweeps_out};
+  if (cudaLaunchCooperativeKernel((void*)sym_eig_coop_kernel, grid, 256, args, smem, st) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  ++g_launches;
+  return true;
 }
 
 }  // namespace tsg
