@@ -126,6 +126,12 @@ int64_t tsg_metrics_count(tsg_stream* h);
 int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out);
 int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out);
 
+/* Profiling harness: average ms of the fused projection kernel over `reps`
+ * launches on device buffers (flags: 1 skip the residual phase, 2 skip the
+ * cross-warp reduction; results are then not meaningful). */
+int tsg_debug_project(const double* x, int64_t left, int64_t n, int64_t right,
+                      const double* u, int32_t R, double* p, int32_t flags,
+                      int32_t reps, double* ms_out);
 /* Bytes the engine reads back per absorbed slice (decision slot, control
  * block snapshot, metrics record). */
 int64_t tsg_readback_bytes_per_update(void);

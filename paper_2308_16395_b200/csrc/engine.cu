@@ -1419,6 +1419,53 @@ int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tfl
 
 int tsg_debug_isvd_clocks(int64_t* out) { return tsg::read_isvd_clocks(reinterpret_cast<long long*>(out)); }
 
+// Profiling harness: time `reps` launches of the fused projection on device
+// buffers (x: left*n*right, u: n x R column-major, p: left*R*right).
+int tsg_debug_project(const double* x, int64_t left, int64_t n, int64_t right, const double* u,
+                      int32_t R, double* p, int32_t flags, int32_t reps, double* ms_out) {
+  return guarded(nullptr, [&] {
+    cudaStream_t st;
+    ck(cudaStreamCreate(&st), "stream");
+    double* part = nullptr;
+    double* up = nullptr;
+    unsigned* ctr = nullptr;
+    ck(cudaMalloc(&part, sizeof(double) * 2 * kMaxGrid), "malloc");
+    ck(cudaMalloc(&up, sizeof(double) * tsg::upad_size(n, R)), "malloc");
+    ck(cudaMalloc(&ctr, sizeof(unsigned) * 64), "malloc");
+    tsg::launch_pad_u(u, n, R, up, st);
+    ProjArgs a;
+    a.x = x;
+    a.v = ModeView{left, n, right};
+    a.u = u;
+    a.R = R;
+    a.p = p;
+    a.partial = part;
+    a.residual = (flags & 1) ? 0 : 1;
+    a.stream_in = left == 1 ? 1 : 0;
+    a.upad = up;
+    a.debug_skip = flags;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int i = 0; i < reps + 2; ++i) {
+      if (i == 2) cudaEventRecord(e0, st);
+      cudaMemsetAsync(ctr + (i % 64), 0, sizeof(unsigned), st);
+      a.tile_counter = ctr + (i % 64);
+      launch_project(a, st);
+    }
+    cudaEventRecord(e1, st);
+    ck(cudaEventSynchronize(e1), "sync");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    *ms_out = ms / reps;
+    cudaFree(part);
+    cudaFree(up);
+    cudaFree(ctr);
+    cudaStreamDestroy(st);
+    ck(cudaGetLastError(), "kernel");
+  });
+}
+
 int64_t tsg_readback_bytes_per_update(void) {
   return (int64_t)(sizeof(Ctrl) + sizeof(Metrics) + sizeof(SliceCtl));
 }

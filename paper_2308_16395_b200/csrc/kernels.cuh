@@ -75,6 +75,7 @@ struct ProjArgs {
   int stream_in = 0;           // input read once: evict-first loads
   unsigned* tile_counter = nullptr;  // zeroed dynamic tile scheduler (optional)
   const double* upad = nullptr;      // optional pre-padded U image (see pad_u)
+  int debug_skip = 0;                // profiling only: 1 skip phase 2, 2 skip reduction, 4 skip DMMA
 };
 // Pre-padded U image for the DMMA projection kernel: rows padded to a
 // multiple of 8, row pitch 8*ceil(R/8)+4, zero fill. Returns its size in

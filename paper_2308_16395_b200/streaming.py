@@ -93,7 +93,7 @@ EXPORTED = [
     "tsg_estimate_relative_error", "tsg_metrics_count", "tsg_metrics_at", "tsg_last_metrics",
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
-    "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update",
+    "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
 ]
 
 _LIB = None
