@@ -34,16 +34,7 @@ struct Ctrl {
   int r, r_new, degenerate;
   int status;           // 0 ok, 2 coupling drift, 3 numerical
   int sweeps;
-};
-
-// Per-slice decision record, written by the projection stream and read by
-// the ISVD stream, so consecutive slices can be in flight at once.
-struct SliceCtl {
-  double slice_sq;      // ||y||^2
-  double delta;         // tau ||y|| / sqrt(d)  (streaming.cpp:187-188)
-  double res_sq[kMaxD]; // ||E_k||^2 per non-streaming mode
-  int expand_mode;      // first mode whose residual exceeds delta, -1 none
-  int zero_slice;
+  unsigned long long records;  // per-insertion records published so far
 };
 
 struct Metrics {  // mirrors tsg_slice_metrics' device-filled part
@@ -55,6 +46,28 @@ struct Metrics {  // mirrors tsg_slice_metrics' device-filled part
   double trunc_margin;
   int sweeps;
 };
+
+// Per-slice decision record, written by the projection stream and read by
+// the ISVD stream, so consecutive slices can be in flight at once.
+struct SliceCtl {
+  double slice_sq;      // ||y||^2
+  double delta;         // tau ||y|| / sqrt(d)  (streaming.cpp:187-188)
+  double res_sq[kMaxD]; // ||E_k||^2 per non-streaming mode
+  int expand_mode;      // first mode whose residual exceeds delta, -1 none
+  int zero_slice;
+  unsigned long long seq;  // host mirror: decisions published for this parity
+};
+
+// Host-mapped ring of per-insertion records (metrics + control snapshot),
+// filled by the device without a copy call; `done` publishes the count.
+constexpr int kRecRing = 64;
+struct RecRing {
+  Metrics rec[kRecRing];
+  Ctrl ctrl[kRecRing];
+  unsigned long long done;
+};
+
+
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -13,11 +13,13 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -108,63 +110,164 @@ struct tsg_stream {
   cudaEvent_t ev_proj[2] = {nullptr, nullptr}, ev_isvd[2] = {nullptr, nullptr};
   bool ev_isvd_valid[2] = {false, false};
   long long upd_count = 0;
-  // metrics ring: each insertion writes one record + a ctrl snapshot
-  static constexpr int kRing = 8;
-  Metrics* mdev = nullptr;       // device [kRing]
-  Metrics* mhost = nullptr;      // pinned [kRing]
-  Ctrl* cring_h = nullptr;       // pinned [kRing] ctrl snapshots
-  cudaEvent_t ev_rec[kRing] = {};
+  // Host-mapped channels (no copy calls on the per-slice path): decisions
+  // published by decide_kernel, the projection input pointer per parity, and
+  // the per-insertion record ring.
+  SliceCtl* hslot = nullptr;              // mapped [2]
+  SliceCtl* hslot_d = nullptr;
+  unsigned long long* seq_dev = nullptr;  // device [2] decision counters
+  unsigned long long seq_expect[2] = {0, 0};
+  RecRing* ring_h = nullptr;              // mapped
+  RecRing* ring_d = nullptr;
+  unsigned long long rec_read = 0;        // records consumed by the host
   struct Pending {
-    int slot, mask;
+    int mask;
     double wall;
   };
-  std::vector<Pending> pending;  // FIFO, oldest first
-  int ring_next = 0;
+  std::vector<Pending> pending;  // issued insertions not yet drained, oldest first
   int r_exact = 0;               // streaming rank after the last drained insertion
+  Ctrl last_ctrl{};              // control snapshot of the last drained insertion
+  bool have_last_ctrl = false;
   int drift_pending = 0;
   std::vector<tsg_slice_metrics> metrics;
 
-  // phase profiling (TSG_PROFILE)
-  std::vector<cudaEvent_t> ev_pool;
-  std::vector<std::array<cudaEvent_t, 5>> ev_pending;
-  std::array<cudaEvent_t, 5> ev_cur{};
+  // CUDA graphs of the per-slice fast path, one per buffer/pointer set
+  struct GraphEntry {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    long long launches = 0;
+    cudaGraphNode_t xnode = nullptr;  // kernel node reading the slice
+    cudaKernelNodeParams kp{};
+    ProjArgs pa;
+  };
+  cudaGraphNode_t cap_xnode = nullptr;
+  std::map<std::vector<long long>, GraphEntry> graphs;
+  bool use_graphs = std::getenv("TSG_NO_GRAPH") == nullptr;
+  void clear_graphs() {
+    if (graphs.empty()) return;
+    sync();
+    for (auto& kv : graphs) {
+      cudaGraphExecDestroy(kv.second.exec);
+      cudaGraphDestroy(kv.second.graph);
+    }
+    graphs.clear();
+  }
+  // Run `body(capturing)` on stream s_, from a cached graph when enabled;
+  // `x` re-points the captured slice-reading kernel node.
+  template <class F>
+  void run(const std::vector<long long>& key, cudaStream_t s_, F&& body,
+           const double* x = nullptr) {
+    if (!use_graphs) {
+      body(false);
+      return;
+    }
+    auto it = graphs.find(key);
+    if (it == graphs.end()) {
+      if (graphs.size() >= 32) clear_graphs();
+      GraphEntry g;
+      const long long l0 = g_launches;
+      cap_xnode = nullptr;
+      ck(cudaStreamBeginCapture(s_, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
+      try {
+        body(true);
+      } catch (...) {
+        cudaGraph_t tmp = nullptr;
+        cudaStreamEndCapture(s_, &tmp);
+        if (tmp) cudaGraphDestroy(tmp);
+        throw;
+      }
+      ck(cudaStreamEndCapture(s_, &g.graph), "cudaStreamEndCapture");
+      const cudaError_t e = cudaGraphInstantiate(&g.exec, g.graph, 0);
+      if (e != cudaSuccess) cudaGraphDestroy(g.graph);
+      ck(e, "cudaGraphInstantiate");
+      g.launches = g_launches - l0;
+      g_launches = l0;
+      if (x && cap_xnode) {
+        ck(cudaGraphKernelNodeGetParams(cap_xnode, &g.kp), "kernel node params");
+        std::memcpy(&g.pa, g.kp.kernelParams[0], sizeof(ProjArgs));
+        g.xnode = cap_xnode;
+      } else if (x) {
+        fail(TSG_EDEVICE, "graph capture: slice-reading kernel node not found");
+      }
+      it = graphs.emplace(key, g).first;
+    }
+    GraphEntry& ge = it->second;
+    if (ge.xnode && ge.pa.x != x) {
+      ge.pa.x = x;
+      void* args[1] = {&ge.pa};
+      cudaKernelNodeParams kp = ge.kp;
+      kp.kernelParams = args;
+      kp.extra = nullptr;
+      ck(cudaGraphExecKernelNodeSetParams(ge.exec, ge.xnode, &kp), "graph node update");
+    }
+    ck(cudaGraphLaunch(ge.exec, s_), "cudaGraphLaunch");
+    g_launches += it->second.launches;
+  }
+  void wait_ev(cudaStream_t s_, cudaEvent_t e, bool cap) {
+    ck(cudaStreamWaitEvent(s_, e, cap ? cudaEventWaitExternal : 0), "cudaStreamWaitEvent");
+  }
+  void record_ev(cudaEvent_t e, cudaStream_t s_, bool cap) {
+    ck(cudaEventRecordWithFlags(e, s_, cap ? cudaEventRecordExternal : 0), "cudaEventRecord");
+  }
+
+  // Spin on a host-mapped flag; surfaces device faults and lost results.
+  template <class Pred>
+  void spin(Pred ready, const char* what) {
+    for (unsigned it = 1;; ++it) {
+      if (ready()) return;
+      if ((it & 255) == 0) {
+        const cudaError_t e1 = cudaStreamQuery(st), e2 = cudaStreamQuery(si);
+        if (e1 != cudaSuccess && e1 != cudaErrorNotReady) ck(e1, what);
+        if (e2 != cudaSuccess && e2 != cudaErrorNotReady) ck(e2, what);
+        if (e1 == cudaSuccess && e2 == cudaSuccess) {
+          std::atomic_thread_fence(std::memory_order_seq_cst);
+          if (ready()) return;
+          fail(TSG_EDEVICE, std::string(what) + ": device result was never published");
+        }
+      }
+    }
+  }
+  unsigned long long rec_done() const {
+    return *reinterpret_cast<const volatile unsigned long long*>(&ring_h->done);
+  }
+  // Wait for the decision of the last projection launched on parity `par`.
+  SliceCtl wait_slot(int par) {
+    const volatile unsigned long long* q = &hslot[par].seq;
+    spin([&] { return *q == seq_expect[par]; }, "slice decision");
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return hslot[par];
+  }
+
+  // phase profiling (TSG_PROFILE): per-slice event sets, reused every
+  // kProfSets slices (by then the slice's work has long completed)
+  static constexpr int kProfSets = 4;
+  cudaEvent_t pev[kProfSets][5] = {};
+  bool pev_live[kProfSets] = {};
+  int cur_q = -1;  // event set of the slice being enqueued (-1: none)
   double prof[6] = {0, 0, 0, 0, 0, 0};
   bool profiling() const { return flags & TSG_PROFILE; }
-  cudaEvent_t ev_get() {
-    if (ev_pool.empty()) {
-      cudaEvent_t e;
-      ck(cudaEventCreate(&e), "cudaEventCreate");
-      return e;
-    }
-    cudaEvent_t e = ev_pool.back();
-    ev_pool.pop_back();
-    return e;
+  void ev_mark(int i, cudaStream_t s_, bool cap) {
+    if (!profiling() || cur_q < 0) return;
+    record_ev(pev[cur_q][i], s_, cap);
   }
-  void ev_mark(int i, cudaStream_t s_) {
-    if (!profiling()) return;
-    ev_cur[i] = ev_get();
-    ck(cudaEventRecord(ev_cur[i], s_), "cudaEventRecord");
+  void resolve_prof(int q) {
+    if (!pev_live[q]) return;
+    pev_live[q] = false;
+    ck(cudaEventSynchronize(pev[q][4]), "cudaEventSynchronize");
+    float a = 0.f, b = 0.f, c = 0.f, g = 0.f;
+    cudaEventElapsedTime(&a, pev[q][0], pev[q][1]);
+    cudaEventElapsedTime(&b, pev[q][1], pev[q][2]);
+    cudaEventElapsedTime(&g, pev[q][2], pev[q][3]);
+    cudaEventElapsedTime(&c, pev[q][3], pev[q][4]);
+    prof[0] += 1;
+    prof[1] += a;
+    prof[2] += b;
+    prof[3] += c;
+    prof[4] += g;
+    prof[5] += 1;
   }
-  void ev_commit() {
-    if (!profiling()) return;
-    ev_pending.push_back(ev_cur);
-  }
-  void ev_resolve() {
-    for (auto& t : ev_pending) {
-      float a = 0.f, b = 0.f, c = 0.f, g = 0.f;
-      cudaEventElapsedTime(&a, t[0], t[1]);
-      cudaEventElapsedTime(&b, t[1], t[2]);
-      cudaEventElapsedTime(&g, t[2], t[3]);
-      cudaEventElapsedTime(&c, t[3], t[4]);
-      prof[0] += 1;
-      prof[1] += a;
-      prof[2] += b;
-      prof[3] += c;
-      prof[4] += g;
-      prof[5] += 1;
-      for (auto e : t) ev_pool.push_back(e);
-    }
-    ev_pending.clear();
+  void resolve_all() {
+    for (int q = 0; q < kProfSets; ++q) resolve_prof(q);
   }
 
   long long cur_bytes = 0, peak_bytes = 0;
@@ -198,14 +301,20 @@ struct tsg_stream {
     for (auto& a : allocs) cudaFree(a.first);
     allocs.clear();
     cur_bytes = 0;
+    for (auto& kv : graphs) {
+      cudaGraphExecDestroy(kv.second.exec);
+      cudaGraphDestroy(kv.second.graph);
+    }
+    graphs.clear();
     if (ctrl_h) cudaFreeHost(ctrl_h);
-    if (mhost) cudaFreeHost(mhost);
-    if (cring_h) cudaFreeHost(cring_h);
     if (slots_h) cudaFreeHost(slots_h);
+    if (hslot) cudaFreeHost(hslot);
+    if (ring_h) cudaFreeHost(ring_h);
     ctrl_h = nullptr;
-    mhost = nullptr;
-    cring_h = nullptr;
     slots_h = nullptr;
+    hslot = nullptr;
+    ring_h = nullptr;
+    ring_d = nullptr;
   }
 
   // all streams
@@ -227,7 +336,7 @@ struct tsg_stream {
     ck(cudaMemcpyAsync(ctrl_h, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
     sync();
     ck(cudaGetLastError(), "kernel");
-    if (!ev_pending.empty()) ev_resolve();
+    if (profiling()) resolve_all();
   }
   // this slice's decision record (projection stream only)
   void pull_slot(int par) {
@@ -305,16 +414,18 @@ struct tsg_stream {
   }
 
   // ---------------------------------------------------- metrics drain
-  // Retire finished insertions in order (all of them when `force`).
+  // Retire published insertions in order (all issued ones when `force`).
   void drain(bool force = true) {
-    while (!pending.empty()) {
+    if (pending.empty()) return;
+    const unsigned long long target = rec_read + pending.size();
+    if (force) spin([&] { return rec_done() >= target; }, "insertion record");
+    const unsigned long long done = rec_done();
+    std::atomic_thread_fence(std::memory_order_acquire);
+    while (rec_read < done && !pending.empty()) {
+      const int pos = (int)(rec_read % kRecRing);
+      const Metrics m = ring_h->rec[pos];
+      const Ctrl cs = ring_h->ctrl[pos];
       const Pending p = pending.front();
-      if (force) {
-        ck(cudaEventSynchronize(ev_rec[p.slot]), "cudaEventSynchronize");
-      } else if (cudaEventQuery(ev_rec[p.slot]) != cudaSuccess) {
-        break;
-      }
-      const Metrics& m = mhost[p.slot];
       tsg_slice_metrics o;
       std::memset(&o, 0, sizeof o);
       o.slice_index = m.slice_index;
@@ -329,10 +440,17 @@ struct tsg_stream {
       o.trunc_margin = m.trunc_margin;
       o.jacobi_sweeps = m.sweeps;
       metrics.push_back(o);
-      r_exact = cring_h[p.slot].r;
-      if (cring_h[p.slot].status != 0) drift_pending = cring_h[p.slot].status;
+      r_exact = cs.r;
+      last_ctrl = cs;
+      have_last_ctrl = true;
+      if (cs.status != 0) drift_pending = cs.status;
+      ++rec_read;
       pending.erase(pending.begin());
     }
+  }
+  // Room in the record ring for one more insertion.
+  void reserve_record() {
+    if (pending.size() + 2 >= (size_t)kRecRing) drain(true);
   }
 
   void check_status() {
@@ -431,6 +549,16 @@ struct tsg_stream {
   // ------------------------------------------------------- projection
   // Projection of y (dims yd, order d-1) along `mode`: P into out,
   // partials into `part`; returns partial count.
+  // Pre-padded U image and tile counters (allocated outside graph capture).
+  void prep_proj(int mode) {
+    if (upad_R[mode] != R[mode]) {
+      dfree(upad[mode]);
+      upad[mode] = dalloc(upad_size(N[mode], (int)R[mode]));
+      launch_pad_u(U[mode], N[mode], (int)R[mode], upad[mode], st);
+      upad_R[mode] = R[mode];
+    }
+    if (!tile_ctr) tile_ctr = reinterpret_cast<unsigned*>(dalloc(kMaxD * 2));
+  }
   int project(const double* y, const long long* yd, int mode, double* out, double* part,
               double* e = nullptr) {
     ProjArgs a;
@@ -443,14 +571,8 @@ struct tsg_stream {
     a.partial = part;
     a.residual = 1;
     a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? 1 : 0;
-    if (upad_R[mode] != R[mode]) {
-      dfree(upad[mode]);
-      upad[mode] = dalloc(upad_size(N[mode], (int)R[mode]));
-      launch_pad_u(U[mode], N[mode], (int)R[mode], upad[mode], st);
-      upad_R[mode] = R[mode];
-    }
+    prep_proj(mode);
     a.upad = upad[mode];
-    if (!tile_ctr) tile_ctr = reinterpret_cast<unsigned*>(dalloc(kMaxD * 2));
     a.tile_counter = tile_ctr + (ctr_next++ % (kMaxD * 4));
     ck(cudaMemsetAsync(a.tile_counter, 0, sizeof(unsigned), st), "memset");
     return launch_project(a, st);
@@ -558,7 +680,9 @@ struct tsg_stream {
   }
 
   // Enqueue the ISVD insertion + core rotation for the slice whose projected
-  // tensor is `b` and whose decisions are in slot `par`, on stream `s_`.
+  // tensor is `b` and whose decisions are in slot `par`, on stream `s_`
+  // (the ISVD stream, from a cached graph, on the fast path; `st` eagerly
+  // after a slow path).
   void enqueue_isvd(const double* b, int par, int mask, cudaStream_t s_, bool commit,
                     std::chrono::steady_clock::time_point t0) {
     drain(false);
@@ -580,16 +704,7 @@ struct tsg_stream {
       evec = dalloc(n);
       evec_n = n;
     }
-    // metrics ring slot: wait for its previous owner to retire
-    const int ms = ring_next;
-    ring_next = (ring_next + 1) % kRing;
-    for (const Pending& p : pending)
-      if (p.slot == ms) {
-        drain(true);
-        break;
-      }
-    if (s_ != st) ck(cudaStreamWaitEvent(s_, ev_proj[par], 0), "cudaStreamWaitEvent");
-    if (commit) launch_commit_modes(ctrl, slots + par, 0, d - 1, 1, s_);
+    reserve_record();
     IsvdBufs B;
     std::memset(&B, 0, sizeof B);
     B.ctrl = ctrl;
@@ -607,22 +722,41 @@ struct tsg_stream {
     B.pgram = pgram;
     B.inner = inner;
     B.partial = ipart;
-    B.metrics = mdev + ms;
+    B.ring = ring_d;
     B.n = n;
-    B.n_d = n_d;
+    B.cap_rows = cap_rows;
     B.capr = capr;
     B.order = d;
     B.r_hint = r_ub;
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
-    ev_mark(3, s_);
-    launch_isvd(B, s_);
-    ev_mark(4, s_);
-    if (mask == 0) ev_commit();
-    ck(cudaMemcpyAsync(cring_h + ms, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, s_), "ctrl D2H");
-    ck(cudaMemcpyAsync(mhost + ms, mdev + ms, sizeof(Metrics), cudaMemcpyDeviceToHost, s_),
-       "metrics D2H");
-    ck(cudaEventRecord(ev_rec[ms], s_), "cudaEventRecord");
-    ck(cudaEventRecord(ev_isvd[par], s_), "cudaEventRecord");
+    const bool graph = (s_ == si);
+    const int q = mask == 0 ? cur_q : -1;
+    auto body = [&](bool cap) {
+      const int saved = cur_q;
+      cur_q = q;
+      if (s_ != st) wait_ev(s_, ev_proj[par], cap);
+      if (commit) launch_commit_modes(ctrl, slots + par, 0, d - 1, 1, s_);
+      ev_mark(3, s_, cap);
+      launch_isvd(B, s_);
+      ev_mark(4, s_, cap);
+      record_ev(ev_isvd[par], s_, cap);
+      cur_q = saved;
+    };
+    if (graph) {
+      std::vector<long long> key = {1, par, commit, (long long)(uintptr_t)b,
+                                    (long long)(uintptr_t)Q, (long long)(uintptr_t)Q2,
+                                    (long long)(uintptr_t)core, (long long)(uintptr_t)core2,
+                                    (long long)(uintptr_t)sigma, (long long)(uintptr_t)sigma2,
+                                    (long long)(uintptr_t)left, (long long)(uintptr_t)left2,
+                                    (long long)(uintptr_t)evec, (long long)(uintptr_t)pgram,
+                                    (long long)(uintptr_t)inner, (long long)(uintptr_t)ipart,
+                                    n, cap_rows, capr, B.r_hint, d, q};
+      for (int k = 0; k + 1 < d; ++k) key.push_back(R[k]);
+      run(key, s_, body);
+    } else {
+      body(false);
+    }
+    if (q >= 0 && profiling()) pev_live[q] = true;
     ev_isvd_valid[par] = true;
     std::swap(Q, Q2);
     std::swap(core, core2);
@@ -630,75 +764,102 @@ struct tsg_stream {
     std::swap(left, left2);
     ++n_d;
     ++insertions_host;
-    pending.push_back(Pending{ms, mask,
-                              std::chrono::duration<double, std::milli>(
-                                  std::chrono::steady_clock::now() - t0).count()});
+    pending.push_back(Pending{mask, std::chrono::duration<double, std::milli>(
+                                        std::chrono::steady_clock::now() - t0).count()});
   }
 
   // A slice whose projections are enqueued but whose decision (basis growth,
   // zero slice) has not been acted on yet.
   struct Pend {
     int par = 0;
+    int q = -1;                 // profiling event set
     const double* y = nullptr;  // device input (caller buffer or staging)
     const double* b = nullptr;  // projected tensor
     std::chrono::steady_clock::time_point t0;
-    std::array<cudaEvent_t, 3> ev{};
   };
   Pend prev;
   bool have_prev = false;
   double* stage[2] = {nullptr, nullptr};  // host-slice staging per parity
 
+  // Mode projections + decision of one slice on `st` (a cached graph: the
+  // input pointer is read by the mode-0 kernel from mapped memory; the
+  // decision is published to mapped memory with a sequence number).
   void enqueue_proj(const double* y, Pend& p) {
     const int par = p.par;
     ensure_pipe();
-    // this parity's buffers and slot were last read by the insertion two slices ago
-    if (ev_isvd_valid[par]) ck(cudaStreamWaitEvent(st, ev_isvd[par], 0), "cudaStreamWaitEvent");
-    long long yd[kMaxD];
-    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
-    DecideArgs da;
-    std::memset(&da, 0, sizeof da);
-    da.slot = slots + par;
-    da.nmodes = d - 1;
-    da.tau = tau;
-    da.order = d;
-    da.partial = partial;
-    const double* cur = y;
-    int off = 0;
+    ensure_partial(1);
+    for (int k = 0; k + 1 < d; ++k) prep_proj(k);
+    if (p.q >= 0 && profiling()) resolve_prof(p.q);
+    auto body = [&](bool cap) {
+      const int saved = cur_q;
+      cur_q = p.q;
+      wait_ev(st, ev_isvd[par], cap);  // buffers + slot last read by the insertion 2 slices ago
+      wait_ev(st, ev_h2d[par], cap);   // staged host slice
+      long long yd[kMaxD];
+      for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+      DecideArgs da;
+      std::memset(&da, 0, sizeof da);
+      da.slot = slots + par;
+      da.host_slot = hslot_d + par;
+      da.seq_counter = seq_dev + par;
+      da.nmodes = d - 1;
+      da.tau = tau;
+      da.order = d;
+      da.partial = partial;
+      const double* cur = y;
+      int off = 0;
+      for (int k = 0; k + 1 < d; ++k) {
+        double* out = pw[par][k & 1];
+        da.off[k] = off;
+        if (k == 0) ev_mark(0, st, cap);
+        da.cnt[k] = project(cur, yd, k, out, partial + off);
+        if (k == 0 && cap) {
+          // the mode-0 kernel node: its input pointer is re-pointed per launch
+          cudaStreamCaptureStatus cs;
+          const cudaGraphNode_t* deps = nullptr;
+          size_t nd = 0;
+          ck(cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd), "capture info");
+          cap_xnode = nd == 1 ? deps[0] : nullptr;
+        }
+        if (k == 0) ev_mark(1, st, cap);
+        off += 2 * da.cnt[k];
+        yd[k] = R[k];
+        cur = out;
+      }
+      da.first_mode = 0;
+      launch_decide(da, st);
+      ev_mark(2, st, cap);
+      record_ev(ev_proj[par], st, cap);
+      cur_q = saved;
+    };
+    std::vector<long long> key = {0, par, d, (long long)(uintptr_t)pw[par][0],
+                                  (long long)(uintptr_t)pw[par][1], (long long)(uintptr_t)partial,
+                                  (long long)(uintptr_t)tile_ctr, profiling() ? p.q : -1};
     for (int k = 0; k + 1 < d; ++k) {
-      double* out = pw[par][k & 1];
-      da.off[k] = off;
-      if (k == 0) ev_mark(0, st);
-      da.cnt[k] = project(cur, yd, k, out, partial + off);
-      if (k == 0) ev_mark(1, st);
-      off += 2 * da.cnt[k];
-      yd[k] = R[k];
-      cur = out;
+      key.push_back((long long)(uintptr_t)U[k]);
+      key.push_back((long long)(uintptr_t)upad[k]);
+      key.push_back(R[k]);
+      key.push_back(N[k]);
     }
-    da.first_mode = 0;
-    launch_decide(da, st);
-    ev_mark(2, st);
-    p.ev = {ev_cur[0], ev_cur[1], ev_cur[2]};
-    ck(cudaMemcpyAsync(slots_h + par, slots + par, sizeof(SliceCtl), cudaMemcpyDeviceToHost, st),
-       "slot D2H");
-    ck(cudaEventRecord(ev_proj[par], st), "cudaEventRecord");
+    ++seq_expect[par];
+    run(key, st, body, y);
     p.y = y;
-    p.b = cur;
+    p.b = pw[par][(d - 2) & 1];
   }
 
   // Act on a slice's decision. Returns true when the slow path ran (the
   // non-streaming bases may have grown, so later projections must be redone).
   bool complete(Pend& p) {
-    ck(cudaEventSynchronize(ev_proj[p.par]), "cudaEventSynchronize");
-    ck(cudaGetLastError(), "kernel");
-    const SliceCtl& sc = slots_h[p.par];
+    const SliceCtl sc = wait_slot(p.par);
     if (sc.zero_slice || sc.expand_mode >= 0) {
+      if (p.q >= 0) pev_live[p.q] = false;
       update_slow(p.y, p.par, p.t0);
       return true;
     }
-    ev_cur[0] = p.ev[0];
-    ev_cur[1] = p.ev[1];
-    ev_cur[2] = p.ev[2];
+    const int saved = cur_q;
+    cur_q = p.q;
     enqueue_isvd(p.b, p.par, 0, si, true, p.t0);
+    cur_q = saved;
     return false;
   }
 
@@ -706,18 +867,20 @@ struct tsg_stream {
     if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
     Pend cur;
     cur.t0 = std::chrono::steady_clock::now();
+    cur.q = profiling() ? (int)(upd_count % kProfSets) : -1;
     cur.par = (int)(upd_count++ & 1);
     const double* y = y_in;
-    if (mem_kind == TSG_MEM_HOST) {
+    const bool misaligned = (reinterpret_cast<uintptr_t>(y_in) & 15) != 0;
+    if (mem_kind == TSG_MEM_HOST || misaligned) {
       // copy engine stream: the H2D of slice t overlaps compute of slice t-1;
       // staging[par] is free once the projections that read it are done
       if (!stage[cur.par]) stage[cur.par] = dalloc(slice_elems);
       ck(cudaStreamWaitEvent(sc, ev_proj[cur.par], 0), "cudaStreamWaitEvent");
       ck(cudaMemcpyAsync(stage[cur.par], y_in, sizeof(double) * slice_elems,
-                         cudaMemcpyHostToDevice, sc), "slice H2D");
+                         mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                         sc), "slice copy");
       ck(cudaEventRecord(ev_h2d[cur.par], sc), "cudaEventRecord");
       ev_h2d_valid[cur.par] = true;
-      ck(cudaStreamWaitEvent(st, ev_h2d[cur.par], 0), "cudaStreamWaitEvent");
       y = stage[cur.par];
       // the caller's previous host slice has been consumed once its copy ends
       if (ev_h2d_valid[cur.par ^ 1]) ck(cudaEventSynchronize(ev_h2d[cur.par ^ 1]), "h2d sync");
@@ -736,7 +899,12 @@ struct tsg_stream {
     } else {
       complete(cur);
       drain(true);
-      pull_ctrl();
+      if (have_last_ctrl && pending.empty()) {
+        *ctrl_h = last_ctrl;  // the device block as the last insertion left it
+        ck(cudaGetLastError(), "kernel");
+      } else {
+        pull_ctrl();
+      }
       check_status();
     }
   }
@@ -747,25 +915,19 @@ struct tsg_stream {
     sync();
     drain(true);
     pull_ctrl();
-    const SliceCtl sc = slots_h[par];
+    const SliceCtl sc = hslot[par];
     if (sc.zero_slice) {
       launch_commit_modes(ctrl, slots + par, 0, 0, 1, st);
       if (n_d + 1 > cap_rows) grow_rows(n_d + 1);
-      const int ms = ring_next;
-      ring_next = (ring_next + 1) % kRing;
+      reserve_record();
       long long sp[kMaxD] = {0};
       for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
-      launch_zero_slice(ctrl, left, capr, mdev + ms, d, sp, st);
-      ck(cudaMemcpyAsync(cring_h + ms, ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost, st), "ctrl D2H");
-      ck(cudaMemcpyAsync(mhost + ms, mdev + ms, sizeof(Metrics), cudaMemcpyDeviceToHost, st),
-         "metrics D2H");
-      ck(cudaEventRecord(ev_rec[ms], st), "cudaEventRecord");
+      launch_zero_slice(ctrl, slots + par, left, capr, ring_d, d, sp, st);
       ck(cudaEventRecord(ev_isvd[par], st), "cudaEventRecord");
       ev_isvd_valid[par] = true;
       ++n_d;
-      pending.push_back(Pending{ms, 0,
-                                std::chrono::duration<double, std::milli>(
-                                    std::chrono::steady_clock::now() - t0).count()});
+      pending.push_back(Pending{0, std::chrono::duration<double, std::milli>(
+                                       std::chrono::steady_clock::now() - t0).count()});
       return;
     }
     // Re-project from `base` (the input of mode m0), grow the first mode whose
@@ -1005,7 +1167,10 @@ struct tsg_stream {
     evec_n = 0;
     metrics.clear();
     pending.clear();
-    ring_next = 0;
+    rec_read = 0;
+    have_last_ctrl = false;
+    for (auto& l : pev_live) l = false;
+    seq_expect[0] = seq_expect[1] = 0;
     r_exact = 0;
     drift_pending = 0;
     upd_count = 0;
@@ -1026,8 +1191,15 @@ struct tsg_stream {
       if (!ev_proj[i]) ck(cudaEventCreateWithFlags(&ev_proj[i], cudaEventDisableTiming), "event");
       if (!ev_isvd[i]) ck(cudaEventCreateWithFlags(&ev_isvd[i], cudaEventDisableTiming), "event");
     }
-    for (int i = 0; i < kRing; ++i)
-      if (!ev_rec[i]) ck(cudaEventCreateWithFlags(&ev_rec[i], cudaEventDisableTiming), "event");
+    for (auto& set : pev)
+      for (auto& e : set)
+        if (!e) ck(cudaEventCreate(&e), "event");
+    // every cross-stream event starts recorded, so graph wait nodes are valid
+    for (int i = 0; i < 2; ++i) {
+      ck(cudaEventRecord(ev_h2d[i], st), "cudaEventRecord");
+      ck(cudaEventRecord(ev_proj[i], st), "cudaEventRecord");
+      ck(cudaEventRecord(ev_isvd[i], st), "cudaEventRecord");
+    }
     ctrl = reinterpret_cast<Ctrl*>(dalloc((sizeof(Ctrl) + 7) / 8));
     ck(cudaMallocHost(&ctrl_h, sizeof(Ctrl)), "cudaMallocHost");
     std::memset(ctrl_h, 0, sizeof(Ctrl));
@@ -1035,9 +1207,17 @@ struct tsg_stream {
     slots = reinterpret_cast<SliceCtl*>(dalloc(2 * ((sizeof(SliceCtl) + 7) / 8)));
     ck(cudaMallocHost(&slots_h, 2 * sizeof(SliceCtl)), "cudaMallocHost");
     std::memset(slots_h, 0, 2 * sizeof(SliceCtl));
-    mdev = reinterpret_cast<Metrics*>(dalloc(kRing * ((sizeof(Metrics) + 7) / 8)));
-    ck(cudaMallocHost(&mhost, kRing * sizeof(Metrics)), "cudaMallocHost");
-    ck(cudaMallocHost(&cring_h, kRing * sizeof(Ctrl)), "cudaMallocHost");
+    ck(cudaHostAlloc(&hslot, 2 * sizeof(SliceCtl), cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(hslot, 0, 2 * sizeof(SliceCtl));
+    ck(cudaHostAlloc(&ring_h, sizeof(RecRing), cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(ring_h, 0, sizeof(RecRing));
+    void* dp = nullptr;
+    ck(cudaHostGetDevicePointer(&dp, hslot, 0), "cudaHostGetDevicePointer");
+    hslot_d = static_cast<SliceCtl*>(dp);
+    ck(cudaHostGetDevicePointer(&dp, ring_h, 0), "cudaHostGetDevicePointer");
+    ring_d = static_cast<RecRing*>(dp);
+    seq_dev = reinterpret_cast<unsigned long long*>(dalloc(2));
+    ck(cudaMemsetAsync(seq_dev, 0, 2 * sizeof(unsigned long long), st), "memset");
   }
 
   void destroy_streams() {
@@ -1045,9 +1225,9 @@ struct tsg_stream {
       if (ev_proj[i]) cudaEventDestroy(ev_proj[i]);
       if (ev_isvd[i]) cudaEventDestroy(ev_isvd[i]);
     }
-    for (auto& e : ev_rec)
-      if (e) cudaEventDestroy(e);
-    for (auto e : ev_pool) cudaEventDestroy(e);
+    for (auto& set : pev)
+      for (auto& e : set)
+        if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i)
       if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
     if (si) cudaStreamDestroy(si);
@@ -1404,7 +1584,7 @@ int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out) {
 int tsg_profile(tsg_stream* h, double* out, int32_t n, int32_t reset) {
   return guarded(h, [&] {
     h->sync();
-    h->ev_resolve();
+    h->resolve_all();
     for (int i = 0; i < n && i < 6; ++i) out[i] = h->prof[i];
     if (reset)
       for (double& v : h->prof) v = 0.0;

@@ -465,7 +465,19 @@ __device__ void pgram_block(const double* __restrict__ left, long long n_d, int 
   }
 }
 
-__device__ void finalize_record(Ctrl* c, const SliceCtl* sl, double d, double cs, Metrics* rec,
+// Append a record to the host-mapped ring (metrics + control snapshot) and
+// publish it: fields, system fence, then the count.
+__device__ void publish(Ctrl* c, const Metrics& m, RecRing* ring) {
+  const unsigned long long k = c->records;
+  const int pos = (int)(k % kRecRing);
+  ring->rec[pos] = m;
+  c->records = k + 1;
+  ring->ctrl[pos] = *c;
+  __threadfence_system();
+  *reinterpret_cast<volatile unsigned long long*>(&ring->done) = k + 1;
+}
+
+__device__ void finalize_record(Ctrl* c, const SliceCtl* sl, double d, double cs, RecRing* ring,
                                 int order, const SpatialRanks& sr) {
   // one batch of independent loads, then stores (no load-after-store chains)
   const int r_new = c->r_new, status = c->status, sweeps = c->sweeps;
@@ -495,7 +507,7 @@ __device__ void finalize_record(Ctrl* c, const SliceCtl* sl, double d, double cs
   m.expanded_mask = 0;
   m.trunc_margin = margin;
   m.sweeps = sweeps;
-  *rec = m;
+  publish(c, m, ring);
 }
 
 // Row update of Q and the core for rows [i0, i1): Qn = [Q q] W,
@@ -622,7 +634,8 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
   double* sU = sV + 32 * 33;
   TSG_CLK(0);
   // p_gram (old left) for the core rotation
-  pgram_block(B.left, B.n_d, B.capr, r, pg);
+  const long long n_d = c->n_d;
+  pgram_block(B.left, n_d, B.capr, r, pg);
   __syncthreads();
   TSG_CLK(8);
   // Two classical Gram-Schmidt passes (CGS2) split b = Q p + e
@@ -729,22 +742,22 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
   double dacc = 0.0, cacc = 0.0;
   update_rows<RMAX>(c, B.q, B.c, se, B.b, stW, stM, stw, sts, n, threadIdx.x, n, blockDim.x,
                     B.qn, B.cn, dacc, cacc);
-  left_rows(c, B.left, B.n_d, B.capr, B.inner + L.U, B.left_new, threadIdx.x, blockDim.x);
+  left_rows(c, B.left, n_d, B.capr, B.inner + L.U, B.left_new, threadIdx.x, blockDim.x);
   dacc = block_sum(dacc, red);
   cacc = block_sum(cacc, red);
   TSG_CLK(3);
   if (threadIdx.x == 0) {
     SpatialRanks sr;
     for (int k = 0; k < kMaxD; ++k) sr.v[k] = B.spatial_ranks[k];
-    finalize_record(c, B.slot, dacc, cacc, B.metrics, B.order, sr);
+    finalize_record(c, B.slot, dacc, cacc, B.ring, B.order, sr);
     TSG_CLK(9);
   }
 }
 
 // ============================================================ split path
-__global__ void pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left, long long n_d,
-                             int capr, double* pg) {
-  pgram_block(left, n_d, capr, ctrl->r, pg);
+__global__ void pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left, int capr,
+                             double* pg) {
+  pgram_block(left, ctrl->n_d, capr, ctrl->r, pg);
 }
 
 __global__ void __launch_bounds__(256) isvd_pass1_kernel(const Ctrl* ctrl, const double* __restrict__ q,
@@ -932,16 +945,16 @@ __global__ void __launch_bounds__(256) isvd_update_kernel(const Ctrl* ctrl, cons
   }
 }
 
-__global__ void isvd_left_kernel(const Ctrl* ctrl, const double* __restrict__ left, long long n_d,
-                                 int capr, const double* __restrict__ inner,
+__global__ void isvd_left_kernel(const Ctrl* ctrl, const double* __restrict__ left, int capr,
+                                 const double* __restrict__ inner,
                                  double* __restrict__ left_new) {
   const InnerLayout L = inner_layout(capr);
-  left_rows(ctrl, left, n_d, capr, inner + L.U, left_new,
+  left_rows(ctrl, left, ctrl->n_d, capr, inner + L.U, left_new,
             blockIdx.x * (long long)blockDim.x + threadIdx.x, (long long)gridDim.x * blockDim.x);
 }
 
 __global__ void isvd_finalize_kernel(Ctrl* c, const SliceCtl* sl, const double* __restrict__ part,
-                                     int nblk, Metrics* rec, int order, SpatialRanks sr) {
+                                     int nblk, RecRing* ring, int order, SpatialRanks sr) {
   __shared__ double red[32];
   double d = 0.0, cs = 0.0;
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
@@ -950,27 +963,31 @@ __global__ void isvd_finalize_kernel(Ctrl* c, const SliceCtl* sl, const double* 
   }
   d = block_sum(d, red);
   cs = block_sum(cs, red);
-  if (threadIdx.x == 0) finalize_record(c, sl, d, cs, rec, order, sr);
+  if (threadIdx.x == 0) finalize_record(c, sl, d, cs, ring, order, sr);
 }
 
 // ------------------------------------------------------- other entry points
-__global__ void zero_slice_kernel(Ctrl* c, double* left, int capr, Metrics* rec, int order,
-                                  SpatialRanks sr) {
+__global__ void zero_slice_kernel(Ctrl* c, const SliceCtl* sl, double* left, int capr,
+                                  RecRing* ring, int order, SpatialRanks sr) {
   const long long nd = c->n_d;
   for (int j = threadIdx.x; j < capr; j += blockDim.x) left[nd * capr + j] = 0.0;
   __syncthreads();
   if (threadIdx.x != 0) return;
-  rec->slice_index = nd;
+  (void)sl;
+  Metrics m;
+  m.slice_index = nd;
   c->n_d = nd + 1;
-  for (int k = 0; k + 1 < order; ++k) rec->ranks[k] = sr.v[k];
-  rec->ranks[order - 1] = c->r;
-  rec->slice_norm = 0.0;
-  rec->projected_norm = 0.0;
-  for (int k = 0; k + 1 < order; ++k) rec->mode_residuals[k] = 0.0;
+  for (int k = 0; k < kMaxD; ++k) m.ranks[k] = (k + 1 < order) ? sr.v[k] : 0;
+  m.ranks[order - 1] = c->r;
+  m.slice_norm = 0.0;
+  m.projected_norm = 0.0;
+  for (int k = 0; k < kMaxD; ++k) m.mode_residuals[k] = 0.0;
   const double booked = c->squared_error + c->nonstream_discarded_sq;
-  rec->error_estimate = c->total_input_sq <= 0.0 ? 0.0 : sqrt(fmax(booked, 0.0) / c->total_input_sq);
-  rec->trunc_margin = 0.0;
-  rec->sweeps = 0;
+  m.error_estimate = c->total_input_sq <= 0.0 ? 0.0 : sqrt(fmax(booked, 0.0) / c->total_input_sq);
+  m.expanded_mask = 0;
+  m.trunc_margin = 0.0;
+  m.sweeps = 0;
+  publish(c, m, ring);
 }
 
 __global__ void init_isvd_kernel(Ctrl* c, const double* __restrict__ core, long long n, int r,
@@ -1075,7 +1092,7 @@ void launch_isvd(const IsvdBufs& B, cudaStream_t st) {
   double* part3 = part2 + (long long)nb * (capr + 1);
   double* part4 = part3 + nb;
   const InnerLayout L = inner_layout(capr);
-  pgram_kernel<<<1, 256, 0, st>>>(B.ctrl, B.left, B.n_d, capr, B.inner + L.pg);
+  pgram_kernel<<<1, 256, 0, st>>>(B.ctrl, B.left, capr, B.inner + L.pg);
   isvd_pass1_kernel<<<nb, 256, 0, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr, part1);
   isvd_pass2_kernel<<<nb, 256, sizeof(double) * capr, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr,
                                                             nb, part1, B.e, part2);
@@ -1112,17 +1129,17 @@ void launch_isvd(const IsvdBufs& B, cudaStream_t st) {
   else
     isvd_update_kernel<0><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
                                               capr, B.qn, B.cn, part4);
-  isvd_left_kernel<<<grid_for((B.n_d + 1) * capr), 256, 0, st>>>(B.ctrl, B.left, B.n_d, capr,
-                                                                  B.inner, B.left_new);
-  isvd_finalize_kernel<<<1, 256, 0, st>>>(B.ctrl, B.slot, part4, gu, B.metrics, B.order, sr);
+  isvd_left_kernel<<<grid_for(B.cap_rows * capr), 256, 0, st>>>(B.ctrl, B.left, capr, B.inner,
+                                                                 B.left_new);
+  isvd_finalize_kernel<<<1, 256, 0, st>>>(B.ctrl, B.slot, part4, gu, B.ring, B.order, sr);
   g_launches += 8;
 }
 
-void launch_zero_slice(Ctrl* ctrl, double* left, int capr, Metrics* rec, int order,
-                       const long long* spatial, cudaStream_t st) {
+void launch_zero_slice(Ctrl* ctrl, const SliceCtl* slot, double* left, int capr, RecRing* ring,
+                       int order, const long long* spatial, cudaStream_t st) {
   SpatialRanks sr;
   for (int k = 0; k < kMaxD; ++k) sr.v[k] = spatial[k];
-  zero_slice_kernel<<<1, 256, 0, st>>>(ctrl, left, capr, rec, order, sr);
+  zero_slice_kernel<<<1, 256, 0, st>>>(ctrl, slot, left, capr, ring, order, sr);
   ++g_launches;
 }
 

@@ -76,6 +76,8 @@ struct ProjArgs {
   unsigned* tile_counter = nullptr;  // zeroed dynamic tile scheduler (optional)
   const double* upad = nullptr;      // optional pre-padded U image (see pad_u)
   int debug_skip = 0;                // profiling only: 1 skip phase 2, 2 skip reduction, 4 skip DMMA
+  int karg0 = 0, karg1 = 0;  // kernel-specific integers (kernels take one ProjArgs parameter so
+                             // a graph node's input pointer can be re-pointed in place)
 };
 // Pre-padded U image for the DMMA projection kernel: rows padded to a
 // multiple of 8, row pitch 8*ceil(R/8)+4, zero fill. Returns its size in
@@ -92,6 +94,8 @@ void launch_sumsq(const double* x, long long n, double* out, double* scratch,
 // --------------------------------------------------------- streaming step
 struct DecideArgs {
   SliceCtl* slot;
+  SliceCtl* host_slot = nullptr;          // mapped host mirror (with seq)
+  unsigned long long* seq_counter = nullptr;  // device counter for host_slot->seq
   const double* partial;     // concatenated partial pairs
   int off[kMaxD], cnt[kMaxD];
   int nmodes;                // d-1
@@ -126,9 +130,9 @@ struct IsvdBufs {
   double* pgram;       // capr*capr
   double* inner;       // scratch for the inner SVD (see engine)
   double* partial;     // per-CTA partials
-  Metrics* metrics;    // record slot for this slice
+  RecRing* ring;       // mapped host ring of per-insertion records
   long long n;
-  long long n_d;       // rows of left before the insertion
+  long long cap_rows;  // left capacity (n_d itself is read from ctrl)
   int capr;
   int order;
   int r_hint;          // streaming rank before the insertion (host mirror)
@@ -139,7 +143,7 @@ int isvd_inner_scratch(int capr);
 int read_isvd_clocks(long long* out);
 
 // Zero slice (streaming.cpp:171-185).
-void launch_zero_slice(Ctrl* ctrl, double* left, int capr, Metrics* rec,
+void launch_zero_slice(Ctrl* ctrl, const SliceCtl* slot, double* left, int capr, RecRing* ring,
                        int order, const long long* spatial, cudaStream_t st);
 
 // stream_init helpers

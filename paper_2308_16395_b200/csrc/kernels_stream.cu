@@ -18,9 +18,10 @@ inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 // Generic fused projection (any mode): tile = BC mode-k fibres staged in
 // shared memory together with U; P = U^T X_tile, then E = X - U P and the
 // squared norms (streaming.cpp:128-133, tensor.cpp:106-162).
-__global__ void __launch_bounds__(256) project_kernel(ProjArgs a, int BC, int u_smem) {
+__global__ void __launch_bounds__(256) project_kernel(ProjArgs a) {
   extern __shared__ double sm[];
   __shared__ double red[32];
+  const int BC = a.karg0, u_smem = a.karg1;
   const long long left = a.v.left, N = a.v.n, right = a.v.right;
   const int R = a.R;
   const long long cols = left * right;
@@ -139,6 +140,19 @@ __global__ void decide_kernel(DecideArgs a) {
     if (em < 0 && !(sqrt(res[k]) <= c->delta)) em = k;  // streaming.cpp:135
   }
   c->expand_mode = em;
+  if (a.host_slot) {
+    // publish to the host without a copy call: fields, fence, then the count
+    SliceCtl* h = a.host_slot;
+    h->slice_sq = c->slice_sq;
+    h->delta = c->delta;
+    for (int k = 0; k < kMaxD; ++k) h->res_sq[k] = c->res_sq[k];
+    h->expand_mode = em;
+    h->zero_slice = c->zero_slice;
+    const unsigned long long q = *a.seq_counter + 1;
+    *a.seq_counter = q;
+    __threadfence_system();
+    *reinterpret_cast<volatile unsigned long long*>(&h->seq) = q;
+  }
 }
 
 __global__ void commit_modes_kernel(Ctrl* c, const SliceCtl* s, int m0, int m1, int with_total) {
@@ -229,7 +243,10 @@ int launch_project(const ProjArgs& a, cudaStream_t st) {
   const long long ntiles = (cols + bc - 1) / bc;
   long long grid = ntiles < 148 ? ntiles : 148;
   if (grid < 1) grid = 1;
-  project_kernel<<<(int)grid, 256, smem, st>>>(a, (int)bc, u_smem);
+  ProjArgs b = a;
+  b.karg0 = (int)bc;
+  b.karg1 = u_smem;
+  project_kernel<<<(int)grid, 256, smem, st>>>(b);
   ++g_launches;
   return (int)grid;
 }

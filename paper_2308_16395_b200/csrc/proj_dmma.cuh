@@ -89,7 +89,7 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned pari
 // pairs it later reads, so no barrier guards the ring).
 template <int RT, int MC, int GM, int STAGES, int NW = 8>
 __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb(RT, MC, GM) : 2))
-    proj_dmma_kernel(ProjArgs a, int streaming_in) {
+    proj_dmma_kernel(ProjArgs a) {
   extern __shared__ double sm[];
   __shared__ double sred[32];
   constexpr int RPAD = 8 * RT + 4;
@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const long long ntiles = (cols + 8 * MC - 1) / (8 * MC);
+  const int streaming_in = a.karg0;
   const double* __restrict__ x = a.x;
 
   double X[MC][GM][2], Xn[MC][GM][2];
@@ -405,7 +406,9 @@ inline int launch_t(const ProjArgs& a, int streaming_in, cudaStream_t st) {
   const long long slots = (long long)(kNumSMs - 1) *
                           (STAGES > 0 ? 1 : (NW == 8 ? pick_minb(RT, MC, GM) : 2));
   const int grid = (int)(ntiles < slots ? (ntiles < 1 ? 1 : ntiles) : slots);
-  proj_dmma_kernel<RT, MC, GM, STAGES, NW><<<grid, 32 * NW, smem, st>>>(a, streaming_in);
+  ProjArgs b = a;
+  b.karg0 = streaming_in;
+  proj_dmma_kernel<RT, MC, GM, STAGES, NW><<<grid, 32 * NW, smem, st>>>(b);
   return grid;
 }
 
@@ -417,7 +420,8 @@ inline int launch_t(const ProjArgs& a, int streaming_in, cudaStream_t st) {
 // (load latency, not bandwidth, limited the register-prefetch path). The
 // math is the same two-phase DMMA scheme as proj_dmma_kernel.
 template <int RT, int MC, int GM, bool WE, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a, int NS) {
+__global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
+  const int NS = a.karg0;
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double sred[32];
   constexpr int RPAD = 8 * RT + 4;
@@ -434,12 +438,13 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a, int NS
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = lane >> 2, t = lane & 3;
   const long long ntiles = (cols + BN - 1) / BN;
+  const double* xsrc = a.x;
   auto issue = [&](long long tl, int stage) {
     const long long c0 = tl * BN;
     const long long nc = (cols - c0) < BN ? (cols - c0) : BN;
     const unsigned bytes = (unsigned)(nc * N * 8);
     mbar_expect_tx(&bar[stage], bytes);
-    bulk_g2s(ring + (long long)stage * BN * N, a.x + c0 * N, bytes, &bar[stage]);
+    bulk_g2s(ring + (long long)stage * BN * N, xsrc + c0 * N, bytes, &bar[stage]);
   };
   if (threadIdx.x == 0) {
     for (int s_ = 0; s_ < NS; ++s_) mbar_init(&bar[s_], 1);
@@ -630,7 +635,9 @@ inline int launch0_t(const ProjArgs& a, cudaStream_t st) {
   const long long ntiles = (a.v.right + 8 * MC - 1) / (8 * MC);
   const long long slots = (long long)(kNumSMs - 1) * MINB;  // one SM for the insertion kernel
   const int grid = (int)(ntiles < slots ? (ntiles < 1 ? 1 : ntiles) : slots);
-  proj0_tma_kernel<RT, MC, GM, WE, MINB><<<grid, 256, smem, st>>>(a, NS);
+  ProjArgs b = a;
+  b.karg0 = NS;
+  proj0_tma_kernel<RT, MC, GM, WE, MINB><<<grid, 256, smem, st>>>(b);
   return grid;
 }
 

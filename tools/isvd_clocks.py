@@ -7,9 +7,14 @@ import cases
 import paper_2308_16395_b200.streaming as S
 L = S.load_library()
 name = sys.argv[1] if len(sys.argv) > 1 else "c3_40"
-case = cases.STREAM_CASES[name]()
+if name in ("c2", "c3", "c5"):
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.CONFIGS[name]
+    case = cases.config_case(cfg, n_slices=cfg.n_init + 8)
+else:
+    case = cases.STREAM_CASES[name]()
 st = S.stream_init(case.init_flat, case.tau, dims=case.init_dims)
-for s in case.slices[:6]:
+for s in case.slices[:8]:
     st.stream_update(s)
 c = np.zeros(16, dtype=np.int64)
 L.tsg_debug_isvd_clocks(c.ctypes.data_as(ctypes.c_void_p))
