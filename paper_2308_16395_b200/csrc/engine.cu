@@ -92,6 +92,7 @@ struct tsg_stream {
   double* pgram = nullptr;
   double* inner = nullptr;
   unsigned* tile_ctr = nullptr;  // dynamic tile-scheduler counters
+  unsigned* tail_done = nullptr;  // fused tail arrival counter
   double* upad[kMaxD] = {nullptr};  // pre-padded U_k images (proj_dmma smem layout)
   long long upad_R[kMaxD] = {0};    // rank the image was built for
   unsigned ctr_next = 0;
@@ -141,6 +142,28 @@ struct tsg_stream {
     ProjArgs pa;
   };
   cudaGraphNode_t cap_xnode = nullptr;
+  unsigned long long* tail_clk = nullptr;  // TSG_TAIL_CLK debug stamps
+  void dump_tail_clk() {
+    if (!tail_clk) return;
+    std::vector<unsigned long long> h(16 * kMaxGrid);
+    cudaMemcpy(h.data(), tail_clk, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ULL;
+    int nb = 0;
+    for (int b = 0; b < kMaxGrid; ++b)
+      if (h[b * 16]) {
+        t0 = std::min(t0, h[b * 16]);
+        nb = b + 1;
+      }
+    for (int i = 0; i < 16; ++i) {
+      unsigned long long lo = ~0ULL, hi = 0;
+      for (int b = 0; b < nb; ++b)
+        if (h[b * 16 + i] >= t0) {
+          lo = std::min(lo, h[b * 16 + i]);
+          hi = std::max(hi, h[b * 16 + i]);
+        }
+      if (hi) std::fprintf(stderr, "tail stamp %2d: min %8.2f us  max %8.2f us\n", i, (lo - t0) * 1e-3, (hi - t0) * 1e-3);
+    }
+  }
   std::map<std::vector<long long>, GraphEntry> graphs;
   bool use_graphs = std::getenv("TSG_NO_GRAPH") == nullptr;
   void clear_graphs() {
@@ -350,12 +373,28 @@ struct tsg_stream {
   }
 
   long long n_rows() const { return prod(R, d - 1); }
+  // partial-sum layout: per-mode pairs from the projection kernels, then the
+  // fused tail's per-CTA partials
+  static constexpr long long kTailPart = 2LL * kMaxGrid * (kMaxD + 1);
+  bool use_tail = std::getenv("TSG_NO_TAIL") == nullptr;
+  // First mode handled by the fused tail kernel (d-1: none; the tail then
+  // only decides): trailing modes with small inputs.
+  int tail_start() const {
+    int m = d - 1;
+    for (int k = d - 2; k >= 1; --k) {
+      long long in = 1;
+      for (int j = 0; j < d - 1; ++j) in *= (j < k ? R[j] : N[j]);
+      if (!tail_eligible(N[k], R[k]) || in > (2LL << 20)) break;
+      m = k;
+    }
+    return m;
+  }
 
   // --------------------------------------------------------- buffers
   // Partials for every mode plus one spare region, allocated once so that
   // pointers captured by enqueued kernels stay valid.
   void ensure_partial(long long n) {
-    const long long need = std::max(n, 2LL * kMaxGrid * (kMaxD + 1) + 64);
+    const long long need = std::max(n, kTailPart + (long long)kMaxD * kMaxGrid + 64);
     if (need <= partial_cap) return;
     if (partial) sync();
     dfree(partial);
@@ -558,6 +597,10 @@ struct tsg_stream {
       upad_R[mode] = R[mode];
     }
     if (!tile_ctr) tile_ctr = reinterpret_cast<unsigned*>(dalloc(kMaxD * 2));
+    if (!tail_done) {
+      tail_done = reinterpret_cast<unsigned*>(dalloc(1));
+      ck(cudaMemsetAsync(tail_done, 0, 8, st), "memset");
+    }
   }
   int project(const double* y, const long long* yd, int mode, double* out, double* part,
               double* e = nullptr) {
@@ -808,7 +851,8 @@ struct tsg_stream {
       da.partial = partial;
       const double* cur = y;
       int off = 0;
-      for (int k = 0; k + 1 < d; ++k) {
+      const int m0 = use_tail ? tail_start() : d - 1;
+      for (int k = 0; k < (use_tail ? m0 : d - 1); ++k) {
         double* out = pw[par][k & 1];
         da.off[k] = off;
         if (k == 0) ev_mark(0, st, cap);
@@ -827,7 +871,34 @@ struct tsg_stream {
         cur = out;
       }
       da.first_mode = 0;
-      launch_decide(da, st);
+      if (use_tail) {
+        TailArgs ta;
+        std::memset(&ta, 0, sizeof ta);
+        ta.x = cur;
+        for (int k = m0; k + 1 < d; ++k) {
+          ta.out[k] = pw[par][k & 1];
+          ta.u[k] = U[k];
+          ta.N[k] = N[k];
+          ta.R[k] = (int)R[k];
+          ta.left[k] = prod(R, k);
+          ta.right[k] = prod(N + k + 1, d - 2 - k);
+        }
+        ta.m0 = m0;
+        ta.m1 = d - 1;
+        ta.part = partial + kTailPart;
+        ta.done = tail_done;
+        ta.da = da;
+        if (std::getenv("TSG_TAIL_CLK")) {
+          if (!tail_clk) {
+            tail_clk = reinterpret_cast<unsigned long long*>(dalloc(16 * kMaxGrid));
+            cudaMemset(tail_clk, 0, 16 * kMaxGrid * 8);
+          }
+          ta.clk = tail_clk;
+        }
+        if (launch_tail(ta, st) < 0) fail(TSG_EDEVICE, "fused tail kernel launch failed");
+      } else {
+        launch_decide(da, st);
+      }
       ev_mark(2, st, cap);
       record_ev(ev_proj[par], st, cap);
       cur_q = saved;
@@ -844,7 +915,7 @@ struct tsg_stream {
     ++seq_expect[par];
     run(key, st, body, y);
     p.y = y;
-    p.b = pw[par][(d - 2) & 1];
+    p.b = d >= 2 ? pw[par][(d - 2) & 1] : nullptr;
   }
 
   // Act on a slice's decision. Returns true when the slow path ran (the
@@ -1006,6 +1077,7 @@ struct tsg_stream {
     drain(true);
     pull_ctrl();
     r_exact = ctrl_h->r;
+    dump_tail_clk();
     check_status();
   }
 
@@ -1157,6 +1229,7 @@ struct tsg_stream {
     core = core2 = Q = Q2 = sigma = sigma2 = left = left2 = nullptr;
     slice = slice_b = w0 = w1 = w2 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
     tile_ctr = nullptr;
+    tail_done = nullptr;
     for (int k = 0; k < kMaxD; ++k) {
       upad[k] = nullptr;
       upad_R[k] = 0;

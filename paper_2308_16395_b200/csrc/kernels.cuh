@@ -104,6 +104,26 @@ struct DecideArgs {
   int order;
 };
 void launch_decide(const DecideArgs& a, cudaStream_t st);
+
+// Fused tail: modes [m0, m1) of one slice (each N_k <= 512, R_k <= 32) and
+// the decision, one cooperative kernel. Mode k reads the output of mode k-1
+// (`x` for k = m0) viewed as (left[k], N[k], right[k]) and writes out[k].
+// da carries the partial pairs of the modes [da.first_mode, m0) projected by
+// the stand-alone kernels. Returns the grid size, or -1 if not applicable.
+struct TailArgs {
+  const double* x;
+  double* out[kMaxD];
+  const double* u[kMaxD];  // U_k, N_k x R_k column-major (ld N_k)
+  long long N[kMaxD], left[kMaxD], right[kMaxD];
+  int R[kMaxD];
+  int m0, m1;
+  double* part;            // kMaxD * grid per-CTA partials
+  unsigned* done;          // arrival counter (zero between launches)
+  DecideArgs da;
+  unsigned long long* clk = nullptr;  // debug: per-CTA globaltimer stamps (16 per CTA)
+};
+bool tail_eligible(long long n, long long r);
+int launch_tail(const TailArgs& t, cudaStream_t st);
 // Ledger commit for modes [m0, m1): nonstream += ||E_k||^2 as rn*rn;
 // with_total adds slice_norm^2 to total_input_sq (streaming.cpp:168-169).
 void launch_commit_modes(Ctrl* ctrl, const SliceCtl* slot, int m0, int m1, int with_total,

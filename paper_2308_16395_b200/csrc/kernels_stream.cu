@@ -7,6 +7,7 @@
 
 #include "kernels.cuh"
 #include "proj_dmma.cuh"
+#include "decide.cuh"
 
 namespace tsg {
 
@@ -127,32 +128,7 @@ __global__ void decide_kernel(DecideArgs a) {
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
-  SliceCtl* c = a.slot;
-  if (a.first_mode == 0) {
-    c->slice_sq = xsq;
-    c->zero_slice = (xsq == 0.0);
-    const double slice_norm = sqrt(xsq);
-    c->delta = a.tau * slice_norm / sqrt((double)a.order);  // streaming.cpp:187-188
-  }
-  int em = -1;
-  for (int k = a.first_mode; k < a.nmodes; ++k) {
-    c->res_sq[k] = res[k];
-    if (em < 0 && !(sqrt(res[k]) <= c->delta)) em = k;  // streaming.cpp:135
-  }
-  c->expand_mode = em;
-  if (a.host_slot) {
-    // publish to the host without a copy call: fields, fence, then the count
-    SliceCtl* h = a.host_slot;
-    h->slice_sq = c->slice_sq;
-    h->delta = c->delta;
-    for (int k = 0; k < kMaxD; ++k) h->res_sq[k] = c->res_sq[k];
-    h->expand_mode = em;
-    h->zero_slice = c->zero_slice;
-    const unsigned long long q = *a.seq_counter + 1;
-    *a.seq_counter = q;
-    __threadfence_system();
-    *reinterpret_cast<volatile unsigned long long*>(&h->seq) = q;
-  }
+  decide_finish(a, xsq, res);
 }
 
 __global__ void commit_modes_kernel(Ctrl* c, const SliceCtl* s, int m0, int m1, int with_total) {
