@@ -93,6 +93,8 @@ struct tsg_stream {
   double* inner = nullptr;
   unsigned* tile_ctr = nullptr;  // dynamic tile-scheduler counters
   unsigned* tail_done = nullptr;  // fused tail arrival counter
+  double* isvd_hand = nullptr;    // grid insertion handoff
+  unsigned* isvd_gsync = nullptr; // grid insertion epoch / flag / arrivals
   double* upad[kMaxD] = {nullptr};  // pre-padded U_k images (proj_dmma smem layout)
   long long upad_R[kMaxD] = {0};    // rank the image was built for
   unsigned ctr_next = 0;
@@ -765,12 +767,16 @@ struct tsg_stream {
     B.pgram = pgram;
     B.inner = inner;
     B.partial = ipart;
+    B.hand = isvd_hand;
+    B.gsync = isvd_gsync;
     B.ring = ring_d;
     B.n = n;
     B.cap_rows = cap_rows;
     B.capr = capr;
     B.order = d;
-    B.r_hint = r_ub;
+    static const int rpad = std::getenv("TSG_RHINT_PAD") ? std::atoi(std::getenv("TSG_RHINT_PAD")) : 0;
+    B.r_hint = std::min(r_ub + rpad, capr - 1);
+    B.commit_modes = commit ? d - 1 : 0;  // ledger commit fused into the insertion
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
     const bool graph = (s_ == si);
     const int q = mask == 0 ? cur_q : -1;
@@ -778,7 +784,6 @@ struct tsg_stream {
       const int saved = cur_q;
       cur_q = q;
       if (s_ != st) wait_ev(s_, ev_proj[par], cap);
-      if (commit) launch_commit_modes(ctrl, slots + par, 0, d - 1, 1, s_);
       ev_mark(3, s_, cap);
       launch_isvd(B, s_);
       ev_mark(4, s_, cap);
@@ -793,6 +798,7 @@ struct tsg_stream {
                                     (long long)(uintptr_t)left, (long long)(uintptr_t)left2,
                                     (long long)(uintptr_t)evec, (long long)(uintptr_t)pgram,
                                     (long long)(uintptr_t)inner, (long long)(uintptr_t)ipart,
+                                    (long long)(uintptr_t)isvd_hand, (long long)(uintptr_t)isvd_gsync,
                                     n, cap_rows, capr, B.r_hint, d, q};
       for (int k = 0; k + 1 < d; ++k) key.push_back(R[k]);
       run(key, s_, body);
@@ -1230,6 +1236,8 @@ struct tsg_stream {
     slice = slice_b = w0 = w1 = w2 = ebuf = kbuf = evec = partial = ipart = pgram = inner = nullptr;
     tile_ctr = nullptr;
     tail_done = nullptr;
+    isvd_hand = nullptr;
+    isvd_gsync = nullptr;
     for (int k = 0; k < kMaxD; ++k) {
       upad[k] = nullptr;
       upad_R[k] = 0;
@@ -1291,6 +1299,11 @@ struct tsg_stream {
     ring_d = static_cast<RecRing*>(dp);
     seq_dev = reinterpret_cast<unsigned long long*>(dalloc(2));
     ck(cudaMemsetAsync(seq_dev, 0, 2 * sizeof(unsigned long long), st), "memset");
+    // grid-insertion handoff + handshake words (zeroed before any insertion)
+    isvd_hand = dalloc(kHandDoubles);
+    isvd_gsync = reinterpret_cast<unsigned*>(dalloc(2));
+    ck(cudaMemsetAsync(isvd_gsync, 0, 16, st), "memset");
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   }
 
   void destroy_streams() {

@@ -17,13 +17,20 @@
 // pair once per sweep); for m = r+1 <= 32 it runs in a single warp with no
 // block barriers.
 #include <cstdio>
+#include <cstdlib>
 
 #include "kernels.cuh"
+namespace tsg {
+__device__ long long g_isvd_clk[32];  // debug phase clocks (thread 0)
+}
+#define SEC_CLK(i)                                         \
+  do {                                                     \
+    if (threadIdx.x == 0) ::tsg::g_isvd_clk[i] = clock64(); \
+  } while (0)
 #include "secular.cuh"
 
 namespace tsg {
 
-__device__ long long g_isvd_clk[16];
 
 // Scratch layout of the inner SVD (all column-major, in the `inner` buffer).
 struct InnerLayout {
@@ -50,7 +57,7 @@ __host__ __device__ inline InnerLayout inner_layout(int capr) {
 int isvd_inner_scratch(int capr) { return (int)inner_layout(capr).total; }
 
 int read_isvd_clocks(long long* out) {
-  return cudaMemcpyFromSymbol(out, g_isvd_clk, sizeof(long long) * 16) == cudaSuccess ? 0 : 4;
+  return cudaMemcpyFromSymbol(out, g_isvd_clk, sizeof(long long) * 32) == cudaSuccess ? 0 : 4;
 }
 
 namespace {
@@ -1051,10 +1058,76 @@ void ensure_smem(K kernel, size_t bytes) {
 
 }  // namespace
 
+#include "isvd_small.cuh"
+#include "isvd_grid.cuh"
+
+namespace {
+template <int RMAX, int RPT, bool QREG = true>
+void launch_small(const IsvdBufs& B0, cudaStream_t st) {
+  IsvdBufs B = B0;
+  const size_t core_bytes = sizeof(double) * (size_t)B.n * (size_t)B.r_hint;
+  B.stage_core = core_bytes <= 120 * 1024 ? 1 : 0;
+  const size_t smem = sizeof(double) * kSmallFixed + (B.stage_core ? core_bytes + 16 : 16);
+  ensure_smem(isvd_small_kernel<RMAX, RPT, QREG>, smem);
+  isvd_small_kernel<RMAX, RPT, QREG><<<1, 512, smem, st>>>(B);
+}
+template <int RMAX>
+void launch_grid(const IsvdBufs& B, cudaStream_t st) {
+  const int G = (int)((B.n + kGridRows - 1) / kGridRows);
+  const size_t smem =
+      sizeof(double) * ((size_t)kSmallFixed + (size_t)B.n + 2 * RMAX * kGridRows + 2);
+  ensure_smem(isvd_grid_kernel<RMAX>, smem);
+  isvd_grid_kernel<RMAX><<<G, 256, smem, st>>>(B);
+}
+// n <= 512 * RPT, r_hint <= RMAX; false when not applicable
+bool try_small(const IsvdBufs& B, cudaStream_t st) {
+  static const bool off = std::getenv("TSG_OLD_ISVD") != nullptr;
+  static const bool small_only = std::getenv("TSG_ISVD_SMALL") != nullptr;
+  if (off || B.r_hint < 1 || B.r_hint > 31) return false;
+  const int rh = B.r_hint;
+  if (!small_only && B.hand && B.gsync && B.n <= kGridMaxRows) {
+    if (rh <= 4) launch_grid<4>(B, st);
+    else if (rh <= 8) launch_grid<8>(B, st);
+    else if (rh <= 12) launch_grid<12>(B, st);
+    else if (rh <= 16) launch_grid<16>(B, st);
+    else if (rh <= 24) launch_grid<24>(B, st);
+    else launch_grid<32>(B, st);
+    return true;
+  }
+  if (B.n <= 512) {
+    if (rh <= 4) launch_small<4, 1>(B, st);
+    else if (rh <= 8) launch_small<8, 1>(B, st);
+    else if (rh <= 12) launch_small<12, 1>(B, st);
+    else if (rh <= 16) launch_small<16, 1>(B, st);
+    else if (rh <= 24) launch_small<24, 1>(B, st);
+    else launch_small<32, 1>(B, st);
+    return true;
+  }
+  if (B.n <= 1024) {
+    if (rh <= 4) launch_small<4, 2>(B, st);
+    else if (rh <= 8) launch_small<8, 2>(B, st);
+    else if (rh <= 12) launch_small<12, 2>(B, st);
+    else if (rh <= 16) launch_small<16, 2>(B, st);
+    else if (rh <= 24) launch_small<24, 2, false>(B, st);
+    else launch_small<32, 2, false>(B, st);
+    return true;
+  }
+  return false;
+}
+}  // namespace
+
 // Fused single-CTA chain when n <= kFusedRows and r + 1 <= 32.
 constexpr long long kFusedRows = 12288;
 
-void launch_isvd(const IsvdBufs& B, cudaStream_t st) {
+void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
+  if (try_small(B0, st)) {
+    g_launches += 1;
+    return;
+  }
+  if (B0.commit_modes > 0) {
+    launch_commit_modes(B0.ctrl, B0.slot, 0, B0.commit_modes, 1, st);
+  }
+  const IsvdBufs& B = B0;
   const long long n = B.n;
   const int capr = B.capr;
   SpatialRanks sr;

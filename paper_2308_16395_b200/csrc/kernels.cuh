@@ -156,9 +156,14 @@ struct IsvdBufs {
   int capr;
   int order;
   int r_hint;          // streaming rank before the insertion (host mirror)
+  int commit_modes;    // > 0: commit this slice's ledgers first (modes [0, commit_modes))
+  int stage_core;      // small path: stage the old core in shared memory
+  double* hand;        // grid path: leader -> followers handoff (kHandDoubles)
+  unsigned* gsync;     // grid path: [0] epoch, [1] flag, [2] arrivals (zero-initialised)
   long long spatial_ranks[kMaxD];
 };
 void launch_isvd(const IsvdBufs& b, cudaStream_t st);
+constexpr int kHandDoubles = 3 * 33 * 33 + 8 * 33 + 16;
 int isvd_inner_scratch(int capr);
 int read_isvd_clocks(long long* out);
 

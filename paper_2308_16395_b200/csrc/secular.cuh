@@ -10,6 +10,9 @@
 #pragma once
 #include <cfloat>
 
+#ifndef SEC_CLK
+#define SEC_CLK(i)
+#endif
 namespace tsg {
 namespace secular {
 
@@ -25,6 +28,17 @@ __device__ __forceinline__ double rcp(double x) {
   e = fma(-x, y, 1.0);
   return fma(y, e, y);
 }
+
+// 1/sqrt(x) for x > 0: hardware approximation + two Newton steps (~1 ulp);
+// a fraction of the cost of the IEEE sqrt / division sequences.
+__device__ __forceinline__ double rsqrt_nr(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  y = y * fma(-h * y, y, 1.5);
+  return y * fma(-h * y, y, 1.5);
+}
+__device__ __forceinline__ double sqrt_nr(double x) { return x > 0.0 ? x * rsqrt_nr(x) : 0.0; }
 
 // f(tau) pieces around origin pole o: returns f, accumulates phi' (without o)
 // and erretm (sum of |terms|).
@@ -303,6 +317,265 @@ __device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scrat
     }
     const double lv = S.lamall[src];
     lam[lane] = lv < 0.0 ? 0.0 : lv;
+  }
+  __syncwarp();
+  return iters;
+}
+
+
+// Register-resident variant for m <= KM: the deflation scan, root solve,
+// Loewner z-hat and eigenvectors run lane-parallel over unrolled register
+// arrays (no shared-memory loops on the critical path). Close poles (which
+// need the sequential Givens deflation) fall back to eig_rank_one. Same
+// outputs and conventions as eig_rank_one.
+template <int N>
+__device__ __forceinline__ double tsum(double (&t)[N]) {  // binary tree, in place
+#pragma unroll
+  for (int w = 1; w < N; w <<= 1) {
+#pragma unroll
+    for (int i = 0; i + w < N; i += 2 * w) t[i] = __dadd_rn(t[i], t[i + w]);
+  }
+  return t[0];
+}
+template <int N>
+__device__ __forceinline__ double tprod(double (&t)[N]) {
+#pragma unroll
+  for (int w = 1; w < N; w <<= 1) {
+#pragma unroll
+    for (int i = 0; i + w < N; i += 2 * w) t[i] = __dmul_rn(t[i], t[i + w]);
+  }
+  return t[0];
+}
+
+// dd[i] = d_i - sigma (origin-shifted poles, padded entries huge with w = 0)
+template <int KM>
+__device__ __forceinline__ double eval_reg(const double (&dd)[KM], const double (&wK)[KM], int o,
+                                           double wo, double tau, double& phi_out, double& dphi,
+                                           double& err) {
+  double q[KM], qr[KM], aq[KM];
+#pragma unroll
+  for (int i = 0; i < KM; ++i) {
+    const double ri = rcp(dd[i] - tau);
+    const double qi = (i == o) ? 0.0 : wK[i] * ri;
+    q[i] = qi;
+    qr[i] = qi * ri;
+    aq[i] = fabs(qi);
+  }
+  const double qo = -wo * rcp(tau);
+  const double phi = tsum<KM>(q);
+  phi_out = phi;
+  dphi = tsum<KM>(qr);
+  err = 1.0 + tsum<KM>(aq) + fabs(qo);
+  return 1.0 + phi + qo;
+}
+
+template <int KM>
+__device__ int solve_root_reg(const double (&dK)[KM], const double (&wK)[KM], const double* sdK,
+                              const double* swK, int K, double wsum, int j, int& o_out,
+                              double& tau_out) {
+  int o;
+  double lo, hi;
+  if (j == 0) {
+    o = 0;
+    lo = 0.0;
+    hi = wsum;
+  } else {
+    const double dj = sdK[j], dj1 = sdK[j - 1];
+    const double mid = 0.5 * (dj + dj1);
+    double t[KM];
+#pragma unroll
+    for (int i = 0; i < KM; ++i) t[i] = (i < K) ? wK[i] * rcp(dK[i] - mid) : 0.0;
+    const double fm = 1.0 + tsum<KM>(t);
+    if (fm >= 0.0) {
+      o = j;
+      lo = 0.0;
+      hi = mid - dj;
+    } else {
+      o = j - 1;
+      lo = mid - dj1;
+      hi = 0.0;
+    }
+  }
+  const double sigma = sdK[o], wo = swK[o];
+  double dd[KM];
+#pragma unroll
+  for (int i = 0; i < KM; ++i) dd[i] = dK[i] - sigma;
+  const bool pos = (o == j);
+  double tau = 0.5 * (lo + hi);
+  if (tau == 0.0) tau = pos ? hi : lo;
+  int it = 0;
+  for (; it < 60; ++it) {
+    double phi, dphi, err;
+    const double f = eval_reg<KM>(dd, wK, o, wo, tau, phi, dphi, err);
+    if (f < 0.0)
+      lo = tau;
+    else
+      hi = tau;
+    if (fabs(f) <= 8.0 * DBL_EPSILON * err) break;
+    const double A = 1.0 + phi - dphi * tau;
+    const double Dd = A * A + 4.0 * dphi * wo;
+    const double sq = sqrt_nr(Dd);
+    // one reciprocal for every branch of the quadratic's stable root
+    double num, den;
+    if (dphi > 0.0) {
+      const bool first = pos ? (A > 0.0) : (A < 0.0);
+      const double as = pos ? A + sq : A - sq;
+      num = first ? 2.0 * wo : (pos ? -A + sq : -A - sq);
+      den = first ? as : 2.0 * dphi;
+    } else {
+      num = wo;
+      den = A;
+    }
+    double t = num * rcp(den);
+    if (!(t > lo && t < hi)) t = 0.5 * (lo + hi);
+    if (fabs(t - tau) <= 2.0 * DBL_EPSILON * fabs(tau)) {
+      tau = t;
+      break;
+    }
+    tau = t;
+    if (hi - lo <= 2.0 * DBL_EPSILON * fmax(fabs(lo), fabs(hi))) break;
+  }
+  o_out = o;
+  tau_out = tau;
+  return it;
+}
+
+template <int KM>
+__device__ int eig_rank_one_fast(int m, const double* d_in, const double* z_in, Scratch S,
+                                 double* lam, double* W, double* sW) {
+  const int lane = threadIdx.x & 31;
+  const double di = lane < m ? d_in[lane] : 0.0;
+  const double zi = lane < m ? z_in[lane] : 0.0;
+  double zn2 = zi * zi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) zn2 += __shfl_xor_sync(FULL, zn2, o);
+  const double d0 = __shfl_sync(FULL, di, 0);
+  const double zn = sqrt_nr(zn2);
+  const double tol = 8.0 * DBL_EPSILON * (d0 + zn2);
+  const bool flag = (lane >= m) || (fabs(zi) * zn <= tol);
+  const unsigned keep = __ballot_sync(FULL, !flag);
+  // close poles between consecutive kept coordinates need sequential Givens
+  // deflation (rare): hand the whole problem to the scalar-lane solver
+  const unsigned below = keep & ((1u << lane) - 1u);
+  const int prev = below ? 31 - __clz(below) : lane;
+  const double dp = __shfl_sync(FULL, di, prev), zp = __shfl_sync(FULL, zi, prev);
+  const bool close = !flag && below &&
+                     fabs(dp - di) * fabs(zp * zi) <= tol * (zp * zp + zi * zi);
+  if (__any_sync(FULL, close) || m > KM) return eig_rank_one(m, d_in, z_in, S, lam, W, sW);
+  SEC_CLK(10);
+  const int K = __popc(keep);
+  const int pos = __popc(below);
+  if (!flag) {
+    S.dK[pos] = di;
+    S.wK[pos] = zi * zi;
+    S.idx[pos] = lane;
+  }
+  double wsum = flag ? 0.0 : zi * zi;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) wsum += __shfl_xor_sync(FULL, wsum, o);
+  __syncwarp();
+  // padded register copies: absent poles sit at +huge with zero weight
+  double dK[KM], wK[KM];
+#pragma unroll
+  for (int i = 0; i < KM; ++i) {
+    dK[i] = i < K ? S.dK[i] : 1e300;
+    wK[i] = i < K ? S.wK[i] : 0.0;
+  }
+  int iters = 0;
+  double my_ls = 0.0, my_lt = 0.0;
+  if (lane < K) {
+    int o;
+    double tau;
+    iters = solve_root_reg<KM>(dK, wK, S.dK, S.wK, K, wsum, lane, o, tau);
+    my_ls = S.dK[o];
+    my_lt = tau;
+    S.ls[lane] = my_ls;
+    S.lt[lane] = tau;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) iters = max(iters, __shfl_xor_sync(FULL, iters, off));
+  __syncwarp();
+  SEC_CLK(11);
+  // Loewner z-hat (lane i < K)
+  double zh_me = 0.0;
+  if (lane < K) {
+    const double dki = S.dK[lane];
+    // own factor first: every factor's tree position is independent of KM
+    double fac[KM + 1];
+    fac[0] = (my_ls - dki) + my_lt;
+#pragma unroll
+    for (int j = 0; j < KM; ++j)
+      fac[j + 1] = (j < K && j != lane) ? ((S.ls[j] - dki) + S.lt[j]) * rcp(dK[j] - dki) : 1.0;
+    const double prod = tprod<KM + 1>(fac);
+    const double mag = sqrt_nr(fabs(prod));
+    zh_me = (z_in[S.idx[lane]] < 0.0) ? -mag : mag;
+    S.zh[lane] = zh_me;
+  }
+  // all eigenvalues: roots (lanes < K) then deflated poles in coordinate order
+  const unsigned defl = (~keep) & ((m >= 32) ? FULL : ((1u << m) - 1u));
+  double lv = 0.0;
+  int kind = -1;
+  if (lane < K) {
+    lv = my_ls + my_lt;
+    kind = lane;
+  } else if (lane < m) {
+    // (lane - K)-th deflated coordinate
+    unsigned mm = defl;
+    for (int c = 0; c < lane - K; ++c) mm &= mm - 1u;
+    const int coord = __ffs(mm) - 1;
+    lv = d_in[coord];  // no rotation: the deflated eigenvalue is the pole
+    kind = 32 + coord;
+  }
+  S.lamall[lane] = lv;
+  __syncwarp();
+  SEC_CLK(12);
+  __shared__ int src_kind[32];
+  src_kind[lane] = kind;
+  if (lane < m) {
+    int rk = 0;
+    for (int j = 0; j < m; ++j) {
+      const double lj = S.lamall[j];
+      if (lj > lv || (lj == lv && j < lane)) ++rk;
+    }
+    S.perm[rk] = lane;
+  }
+  __syncwarp();
+  SEC_CLK(13);
+  if (lane < m) {
+    const int src = S.perm[lane];
+    const int kd = src_kind[src];
+    for (int a = 0; a < m; ++a) sW[a * P + lane] = 0.0;
+    if (kd < 32) {
+      const double lsj = S.ls[kd], ltj = S.lt[kd];
+      double t[KM], t2[KM];
+#pragma unroll
+      for (int i = 0; i < KM; ++i) {
+        t[i] = (i < K) ? S.zh[i] * rcp((dK[i] - lsj) - ltj) : 0.0;
+        t2[i] = t[i] * t[i];
+      }
+      const double inv = rsqrt_nr(tsum<KM>(t2));
+      // sign rule: first coordinate of largest magnitude made positive
+      // (coordinates of the kept poles are increasing in i)
+      double best = -1.0, bv = 0.0;
+#pragma unroll
+      for (int i = 0; i < KM; ++i) {
+        const double v = t[i] * inv;
+        t[i] = v;
+        if (i < K && fabs(v) > best) {
+          best = fabs(v);
+          bv = v;
+        }
+      }
+      const double sgn = bv < 0.0 ? -1.0 : 1.0;
+#pragma unroll
+      for (int i = 0; i < KM; ++i)
+        if (i < K) sW[S.idx[i] * P + lane] = sgn * t[i];
+    } else {
+      sW[(kd - 32) * P + lane] = 1.0;
+    }
+    for (int a = 0; a < m; ++a) W[a + lane * m] = sW[a * P + lane];
+    const double l = S.lamall[src];
+    lam[lane] = l < 0.0 ? 0.0 : l;
   }
   __syncwarp();
   return iters;

@@ -16,8 +16,17 @@ else:
 st = S.stream_init(case.init_flat, case.tau, dims=case.init_dims)
 for s in case.slices[:8]:
     st.stream_update(s)
-c = np.zeros(16, dtype=np.int64)
+c = np.zeros(32, dtype=np.int64)
 L.tsg_debug_isvd_clocks(c.ctypes.data_as(ctypes.c_void_p))
 print(name, st.query()["core_dims"], "pgram", c[8] - c[0], "passes", c[1] - c[8], "pre", c[4] - c[1],
       "secular", c[5] - c[4], "trunc", c[6] - c[5], "U+MGS", c[7] - c[6], "tail", c[2] - c[7],
       "update", c[3] - c[2], "finalize", c[9] - c[3], "total", c[9] - c[0])
+print("small-kernel view: entry/Q", c[8] - c[0], "cgs2", c[1] - c[8], "pre-inner", c[4] - c[1],
+      "inner(warp0)", c[7] - c[4], "barrier", c[2] - c[7], "update+left", c[3] - c[2], "publish", c[9] - c[3],
+      "total", c[9] - c[0])
+print("secular: prologue", c[10] - c[4], "roots", c[11] - c[10], "zhat+lam", c[12] - c[11], "sort", c[13] - c[12],
+      "vectors", c[5] - c[13], "| trunc", c[6] - c[5], "U+MGS", c[7] - c[6])
+print("update rows", c[14] - c[2], "left", c[15] - c[14], "reduce", c[3] - c[15])
+print("M+sw", c[16] - c[2], "wait+sync", c[17] - c[16], "row0", c[18] - c[17], "row1", c[14] - c[18])
+print("grid leader: M+inv", c[16] - c[2], "handoff", c[17] - c[16], "own rows", c[18] - c[17], "left", c[14] - c[18], "reduce+publish", c[9] - c[14])
+print("own rows: e", c[19] - c[17], "chunk0", c[20] - c[19], "chunk1", c[18] - c[20])
