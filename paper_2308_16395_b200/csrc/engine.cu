@@ -104,6 +104,8 @@ struct tsg_stream {
   // ISVD of slice t (stream si); per-parity decision slots and work buffers
   cudaStream_t si = nullptr;
   cudaStream_t sc = nullptr;     // host-to-device copies (overlap with compute)
+  cudaStream_t s2 = nullptr;     // trailing modes + decision (overlap the next mode 0)
+  cudaEvent_t ev_m0[2] = {nullptr, nullptr};
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
   bool ev_h2d_valid[2] = {false, false};
   SliceCtl* slots = nullptr;     // device [2]
@@ -241,10 +243,11 @@ struct tsg_stream {
     for (unsigned it = 1;; ++it) {
       if (ready()) return;
       if ((it & 255) == 0) {
-        const cudaError_t e1 = cudaStreamQuery(st), e2 = cudaStreamQuery(si);
+        const cudaError_t e1 = cudaStreamQuery(st), e2 = cudaStreamQuery(si), e3 = cudaStreamQuery(s2);
         if (e1 != cudaSuccess && e1 != cudaErrorNotReady) ck(e1, what);
         if (e2 != cudaSuccess && e2 != cudaErrorNotReady) ck(e2, what);
-        if (e1 == cudaSuccess && e2 == cudaSuccess) {
+        if (e3 != cudaSuccess && e3 != cudaErrorNotReady) ck(e3, what);
+        if (e1 == cudaSuccess && e2 == cudaSuccess && e3 == cudaSuccess) {
           std::atomic_thread_fence(std::memory_order_seq_cst);
           if (ready()) return;
           fail(TSG_EDEVICE, std::string(what) + ": device result was never published");
@@ -323,6 +326,7 @@ struct tsg_stream {
     if (st) cudaStreamSynchronize(st);
     if (si) cudaStreamSynchronize(si);
     if (sc) cudaStreamSynchronize(sc);
+    if (s2) cudaStreamSynchronize(s2);
     for (auto& a : allocs) cudaFree(a.first);
     allocs.clear();
     cur_bytes = 0;
@@ -345,6 +349,7 @@ struct tsg_stream {
   // all streams
   void sync() {
     if (sc) ck(cudaStreamSynchronize(sc), "cudaStreamSynchronize");
+    if (s2) ck(cudaStreamSynchronize(s2), "cudaStreamSynchronize");
     ck(cudaStreamSynchronize(si), "cudaStreamSynchronize");
     ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
   }
@@ -378,6 +383,8 @@ struct tsg_stream {
   // partial-sum layout: per-mode pairs from the projection kernels, then the
   // fused tail's per-CTA partials
   static constexpr long long kTailPart = 2LL * kMaxGrid * (kMaxD + 1);
+  static constexpr long long kPartStride = kTailPart + (long long)kMaxD * kMaxGrid + 64;
+  DecideArgs last_da[2];  // partial layout of the last captured leading-mode pass
   bool use_tail = std::getenv("TSG_NO_TAIL") == nullptr;
   // First mode handled by the fused tail kernel (d-1: none; the tail then
   // only decides): trailing modes with small inputs.
@@ -396,7 +403,7 @@ struct tsg_stream {
   // Partials for every mode plus one spare region, allocated once so that
   // pointers captured by enqueued kernels stay valid.
   void ensure_partial(long long n) {
-    const long long need = std::max(n, kTailPart + (long long)kMaxD * kMaxGrid + 64);
+    const long long need = std::max(n, 2 * kPartStride);
     if (need <= partial_cap) return;
     if (partial) sync();
     dfree(partial);
@@ -602,6 +609,7 @@ struct tsg_stream {
     if (!tail_done) {
       tail_done = reinterpret_cast<unsigned*>(dalloc(1));
       ck(cudaMemsetAsync(tail_done, 0, 8, st), "memset");
+      ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
   }
   int project(const double* y, const long long* yd, int mode, double* out, double* part,
@@ -839,14 +847,18 @@ struct tsg_stream {
     ensure_partial(1);
     for (int k = 0; k + 1 < d; ++k) prep_proj(k);
     if (p.q >= 0 && profiling()) resolve_prof(p.q);
-    auto body = [&](bool cap) {
+    const int m0 = use_tail ? tail_start() : d - 1;
+    double* part = partial + par * kPartStride;  // per parity: slices t, t+1 overlap
+    // leading (large) modes on st; with the fused tail, the trailing modes and
+    // the decision run on s2 so that they overlap the next slice's mode 0
+    auto mbody = [&](bool cap) {
       const int saved = cur_q;
       cur_q = p.q;
       wait_ev(st, ev_isvd[par], cap);  // buffers + slot last read by the insertion 2 slices ago
       wait_ev(st, ev_h2d[par], cap);   // staged host slice
       long long yd[kMaxD];
       for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
-      DecideArgs da;
+      DecideArgs& da = last_da[par];
       std::memset(&da, 0, sizeof da);
       da.slot = slots + par;
       da.host_slot = hslot_d + par;
@@ -854,15 +866,14 @@ struct tsg_stream {
       da.nmodes = d - 1;
       da.tau = tau;
       da.order = d;
-      da.partial = partial;
+      da.partial = part;
       const double* cur = y;
       int off = 0;
-      const int m0 = use_tail ? tail_start() : d - 1;
-      for (int k = 0; k < (use_tail ? m0 : d - 1); ++k) {
+      for (int k = 0; k < m0; ++k) {
         double* out = pw[par][k & 1];
         da.off[k] = off;
         if (k == 0) ev_mark(0, st, cap);
-        da.cnt[k] = project(cur, yd, k, out, partial + off);
+        da.cnt[k] = project(cur, yd, k, out, part + off);
         if (k == 0 && cap) {
           // the mode-0 kernel node: its input pointer is re-pointed per launch
           cudaStreamCaptureStatus cs;
@@ -877,39 +888,48 @@ struct tsg_stream {
         cur = out;
       }
       da.first_mode = 0;
-      if (use_tail) {
-        TailArgs ta;
-        std::memset(&ta, 0, sizeof ta);
-        ta.x = cur;
-        for (int k = m0; k + 1 < d; ++k) {
-          ta.out[k] = pw[par][k & 1];
-          ta.u[k] = U[k];
-          ta.N[k] = N[k];
-          ta.R[k] = (int)R[k];
-          ta.left[k] = prod(R, k);
-          ta.right[k] = prod(N + k + 1, d - 2 - k);
-        }
-        ta.m0 = m0;
-        ta.m1 = d - 1;
-        ta.part = partial + kTailPart;
-        ta.done = tail_done;
-        ta.da = da;
-        if (std::getenv("TSG_TAIL_CLK")) {
-          if (!tail_clk) {
-            tail_clk = reinterpret_cast<unsigned long long*>(dalloc(16 * kMaxGrid));
-            cudaMemset(tail_clk, 0, 16 * kMaxGrid * 8);
-          }
-          ta.clk = tail_clk;
-        }
-        if (launch_tail(ta, st) < 0) fail(TSG_EDEVICE, "fused tail kernel launch failed");
-      } else {
+      if (!use_tail) {
         launch_decide(da, st);
+        ev_mark(2, st, cap);
+        record_ev(ev_proj[par], st, cap);
+      } else {
+        record_ev(ev_m0[par], st, cap);
       }
-      ev_mark(2, st, cap);
-      record_ev(ev_proj[par], st, cap);
       cur_q = saved;
     };
-    std::vector<long long> key = {0, par, d, (long long)(uintptr_t)pw[par][0],
+    auto tbody = [&](bool cap) {
+      const int saved = cur_q;
+      cur_q = p.q;
+      wait_ev(s2, ev_m0[par], cap);
+      TailArgs ta;
+      std::memset(&ta, 0, sizeof ta);
+      ta.x = pw[par][(m0 - 1) & 1];
+      for (int k = m0; k + 1 < d; ++k) {
+        ta.out[k] = pw[par][k & 1];
+        ta.u[k] = U[k];
+        ta.N[k] = N[k];
+        ta.R[k] = (int)R[k];
+        ta.left[k] = prod(R, k);
+        ta.right[k] = prod(N + k + 1, d - 2 - k);
+      }
+      ta.m0 = m0;
+      ta.m1 = d - 1;
+      ta.part = part + kTailPart;
+      ta.done = tail_done + par;
+      ta.da = last_da[par];
+      if (std::getenv("TSG_TAIL_CLK")) {
+        if (!tail_clk) {
+          tail_clk = reinterpret_cast<unsigned long long*>(dalloc(16 * kMaxGrid));
+          cudaMemset(tail_clk, 0, 16 * kMaxGrid * 8);
+        }
+        ta.clk = tail_clk;
+      }
+      if (launch_tail(ta, s2) < 0) fail(TSG_EDEVICE, "fused tail kernel launch failed");
+      ev_mark(2, s2, cap);
+      record_ev(ev_proj[par], s2, cap);
+      cur_q = saved;
+    };
+    std::vector<long long> key = {0, par, d, m0, (long long)(uintptr_t)pw[par][0],
                                   (long long)(uintptr_t)pw[par][1], (long long)(uintptr_t)partial,
                                   (long long)(uintptr_t)tile_ctr, profiling() ? p.q : -1};
     for (int k = 0; k + 1 < d; ++k) {
@@ -919,7 +939,11 @@ struct tsg_stream {
       key.push_back(N[k]);
     }
     ++seq_expect[par];
-    run(key, st, body, y);
+    run(key, st, mbody, y);
+    if (use_tail) {
+      key[0] = 2;
+      run(key, s2, tbody);
+    }
     p.y = y;
     p.b = d >= 2 ? pw[par][(d - 2) & 1] : nullptr;
   }
@@ -952,7 +976,9 @@ struct tsg_stream {
       // copy engine stream: the H2D of slice t overlaps compute of slice t-1;
       // staging[par] is free once the projections that read it are done
       if (!stage[cur.par]) stage[cur.par] = dalloc(slice_elems);
-      ck(cudaStreamWaitEvent(sc, ev_proj[cur.par], 0), "cudaStreamWaitEvent");
+      // staging[par] is free once the mode-0 pass that read it is done
+      ck(cudaStreamWaitEvent(sc, use_tail ? ev_m0[cur.par] : ev_proj[cur.par], 0),
+         "cudaStreamWaitEvent");
       ck(cudaMemcpyAsync(stage[cur.par], y_in, sizeof(double) * slice_elems,
                          mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                          sc), "slice copy");
@@ -1264,6 +1290,9 @@ struct tsg_stream {
     insertions_host = 0;
     if (!si) ck(cudaStreamCreateWithFlags(&si, cudaStreamNonBlocking), "cudaStreamCreate");
     if (!sc) ck(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking), "cudaStreamCreate");
+    if (!s2) ck(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < 2; ++i)
+      if (!ev_m0[i]) ck(cudaEventCreateWithFlags(&ev_m0[i], cudaEventDisableTiming), "event");
     for (int i = 0; i < 2; ++i) {
       if (!ev_h2d[i]) ck(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming), "event");
       ev_h2d_valid[i] = false;
@@ -1280,6 +1309,7 @@ struct tsg_stream {
       ck(cudaEventRecord(ev_h2d[i], st), "cudaEventRecord");
       ck(cudaEventRecord(ev_proj[i], st), "cudaEventRecord");
       ck(cudaEventRecord(ev_isvd[i], st), "cudaEventRecord");
+      ck(cudaEventRecord(ev_m0[i], st), "cudaEventRecord");
     }
     ctrl = reinterpret_cast<Ctrl*>(dalloc((sizeof(Ctrl) + 7) / 8));
     ck(cudaMallocHost(&ctrl_h, sizeof(Ctrl)), "cudaMallocHost");
@@ -1316,10 +1346,14 @@ struct tsg_stream {
         if (e) cudaEventDestroy(e);
     for (int i = 0; i < 2; ++i)
       if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
+    for (int i = 0; i < 2; ++i)
+      if (ev_m0[i]) cudaEventDestroy(ev_m0[i]);
     if (si) cudaStreamDestroy(si);
     if (sc) cudaStreamDestroy(sc);
+    if (s2) cudaStreamDestroy(s2);
     si = nullptr;
     sc = nullptr;
+    s2 = nullptr;
   }
 
   // ------------------------------------------------------ export/import

@@ -33,7 +33,7 @@ __device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
 }
 
 template <int RMAX>
-__global__ void __launch_bounds__(256, 1) isvd_grid_kernel(IsvdBufs B) {
+__global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
   constexpr int RM = RMAX + 1;
   constexpr int P = 33;
   constexpr int NW = 8;
@@ -62,6 +62,11 @@ __global__ void __launch_bounds__(256, 1) isvd_grid_kernel(IsvdBufs B) {
   unsigned* gs = B.gsync;
   double* hand = B.hand;
   if (leader) TSG_CLK(0);
+  if (leader && tid == 0) {
+    unsigned long long g;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+    g_isvd_clk[24] = (long long)g;
+  }
   if (tid == 0) {
     sh_epoch = *reinterpret_cast<volatile unsigned*>(gs);
     sh_r = c->r;    // c->r and c->n_d change only in the final record (this kernel's end)
@@ -448,6 +453,11 @@ __global__ void __launch_bounds__(256, 1) isvd_grid_kernel(IsvdBufs B) {
     __threadfence_system();
     __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&B.ring->done) = kr + 1;
+    if (lane == 0) {
+      unsigned long long g;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g));
+      g_isvd_clk[25] = (long long)g;
+    }
   }
   if (leader) TSG_CLK(9);
 }

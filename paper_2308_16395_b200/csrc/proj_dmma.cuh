@@ -633,7 +633,14 @@ inline int launch0_t(const ProjArgs& a, cudaStream_t st) {
     attr = cap;
   }
   const long long ntiles = (a.v.right + 8 * MC - 1) / (8 * MC);
-  const long long slots = (long long)(kNumSMs - 1) * MINB;  // one SM for the insertion kernel
+  // leave room for the concurrent tail / insertion kernels
+  static const long long cap_ctas = [] {
+    const char* e = std::getenv("TSG_M0_CTAS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  // default: 8 SMs' worth of slots stay free for the overlapping kernels
+  long long slots = (long long)(kNumSMs - 8) * MINB;
+  if (cap_ctas > 0) slots = cap_ctas;
   const int grid = (int)(ntiles < slots ? (ntiles < 1 ? 1 : ntiles) : slots);
   ProjArgs b = a;
   b.karg0 = NS;
