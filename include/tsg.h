@@ -13,6 +13,9 @@
  *   tsg_import_state    <- tucker::assemble_streaming_state  streaming.hpp:85-87
  *   tsg_export_state    <- StreamingState fields + streaming_factor()
  *                                                            streaming.hpp:34-49
+ *   tsg_shard_setup / tsg_shard_begin / tsg_shard_continue
+ *                       <- stream_update split over G GPUs (no reference
+ *                          counterpart; see the sharded section below)
  *   tsg_metrics_at / tsg_last_metrics
  *                       <- StreamingState::metrics (SliceMetrics, streaming.hpp:13-22)
  *   tsg_sym_eig_desc, tsg_small_svd_truncated, tsg_mode_subspace, tsg_ttm
@@ -125,6 +128,40 @@ double tsg_estimate_relative_error(tsg_stream* h);
 int64_t tsg_metrics_count(tsg_stream* h);
 int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out);
 int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out);
+
+/* ---- Sharded update (one process per GPU).
+ *
+ * The reference has no distributed mode: this splits ONE stream_update
+ * (streaming.hpp:63) across G ranks. Every rank holds the full state (same
+ * tsg_init input on every rank, or tsg_import_state of the same state) and
+ * rows [bounds[g], bounds[g+1]) of the LAST spatial mode s = d-2 of each
+ * slice — a contiguous chunk of the colexicographic slice, passed as a dense
+ * tensor N_0 x ... x N_{s-1} x (bounds[g+1]-bounds[g]).
+ *
+ *   tsg_shard_setup(h, g, G, bounds)            once, after init/import
+ *   per slice:
+ *     tsg_shard_begin(h, slab, mem_kind, &ex)   local projections of modes < s
+ *     while (ex.pending) {
+ *       allgather(ex.send -> ex.recv, ex.count doubles per rank, rank order)
+ *       tsg_shard_continue(h, &ex)
+ *     }
+ *
+ * The exchange buffers are device memory owned by the handle; the collective
+ * must be complete, or enqueued on tsg_cuda_stream(h), when
+ * tsg_shard_continue is called. In steady state there is exactly one
+ * exchange per slice (the compressed local tensor plus partial norms);
+ * growth of a basis k < s adds one more. Every reduction over ranks runs in
+ * rank order on the gathered bytes, so all ranks end bitwise identical. */
+typedef struct {
+  int32_t pending;   /* 1: an allgather is requested; 0: the update is done */
+  int64_t count;     /* doubles contributed by each rank */
+  double* send;      /* device: this rank's count doubles */
+  double* recv;      /* device: world * count doubles, rank g's block at g * count */
+} tsg_exchange;
+
+int tsg_shard_setup(tsg_stream* h, int32_t rank, int32_t world, const int64_t* bounds);
+int tsg_shard_begin(tsg_stream* h, const double* slab, int32_t mem_kind, tsg_exchange* ex);
+int tsg_shard_continue(tsg_stream* h, tsg_exchange* ex);
 
 /* Profiling harness: average ms of the fused projection kernel over `reps`
  * launches on device buffers (flags: 1 skip the residual phase, 2 skip the

@@ -626,8 +626,14 @@ struct tsg_stream {
     a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? 1 : 0;
     prep_proj(mode);
     a.upad = upad[mode];
-    a.tile_counter = tile_ctr + (ctr_next++ % (kMaxD * 4));
-    ck(cudaMemsetAsync(a.tile_counter, 0, sizeof(unsigned), st), "memset");
+    if (shard_world > 0) {
+      // sharded: static tile order, so the partial sums (and every decision
+      // and ledger derived from them) are bitwise identical on all ranks
+      a.tile_counter = nullptr;
+    } else {
+      a.tile_counter = tile_ctr + (ctr_next++ % (kMaxD * 4));
+      ck(cudaMemsetAsync(a.tile_counter, 0, sizeof(unsigned), st), "memset");
+    }
     return launch_project(a, st);
   }
 
@@ -1020,6 +1026,17 @@ struct tsg_stream {
     pull_ctrl();
     const SliceCtl sc = hslot[par];
     if (sc.zero_slice) {
+      zero_slice_path(par, t0);
+      return;
+    }
+    long long yd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+    run_growth(y, yd, 0, sc.expand_mode, sc.delta, par, t0);
+  }
+
+  // streaming.cpp:171-185: a zero left row and a metrics record.
+  void zero_slice_path(int par, std::chrono::steady_clock::time_point t0) {
+    {
       launch_commit_modes(ctrl, slots + par, 0, 0, 1, st);
       if (n_d + 1 > cap_rows) grow_rows(n_d + 1);
       reserve_record();
@@ -1031,12 +1048,17 @@ struct tsg_stream {
       ++n_d;
       pending.push_back(Pending{0, std::chrono::duration<double, std::milli>(
                                        std::chrono::steady_clock::now() - t0).count()});
-      return;
     }
-    // Re-project from `base` (the input of mode m0), grow the first mode whose
-    // residual exceeds delta, continue with the grown tensor.
+  }
+
+  // Basis growth (streaming.cpp:140-151) starting from `base_in`, the input
+  // of mode m0_in with dims yd_in: rebuild the input of mode `em` (the first
+  // mode whose residual exceeds delta), grow it, continue with the grown
+  // tensor, then insert. Slot `par` holds the slice's decision record.
+  void run_growth(const double* base_in, const long long* yd_in, int m0_in, int em, double delta,
+                  int par, std::chrono::steady_clock::time_point t0) {
     long long yd[kMaxD];
-    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = yd_in[k];
     DecideArgs da;
     std::memset(&da, 0, sizeof da);
     da.slot = slots + par;
@@ -1044,10 +1066,8 @@ struct tsg_stream {
     da.tau = tau;
     da.order = d;
     da.partial = partial;
-    const double delta = sc.delta;
-    int em = sc.expand_mode;
-    const double* base = y;
-    int m0 = 0, mask = 0;
+    const double* base = base_in;
+    int m0 = m0_in, mask = 0;
     launch_commit_modes(ctrl, slots + par, 0, em, 1, st);
     const double* b = nullptr;
     while (true) {
@@ -1098,6 +1118,218 @@ struct tsg_stream {
     ensure_pipe();
     enqueue_isvd(b, par, mask, st, false, t0);
     ck(cudaEventRecord(ev_proj[par], st), "cudaEventRecord");
+  }
+
+  // ------------------------------------------------------ sharded update
+  // SURVEY §8(e). Rank `shard_rank` of `shard_world` holds rows
+  // [shard_lo[g], shard_lo[g] + shard_n[g]) of the last spatial mode
+  // s = d-2 of every slice (a contiguous chunk of the colexicographic slice).
+  // Modes 0..s-1 are projected on the local slab; the exchange is ONE
+  // allgather of [partial norm pairs of modes < s | local part of the input
+  // of mode s] (the compressed tensor, R_0..R_{s-1} x N_s/G doubles per rank).
+  // Mode s onwards, the decision and the insertion then run redundantly on
+  // the identical assembled bytes, so all ranks hold bitwise-identical states
+  // without a factor broadcast. Basis growth at a mode k < s (rare) gathers
+  // the input of mode k the same way and grows redundantly.
+  // The host fulfils each exchange (NCCL allgather over NVLink, or any other
+  // transport) between tsg_shard_begin and tsg_shard_continue.
+  int shard_world = 0, shard_rank = 0;
+  long long shard_lo[kMaxShards] = {0}, shard_n[kMaxShards] = {0};
+  double *sh_send = nullptr, *sh_recv = nullptr, *sh_z = nullptr, *sh_stage = nullptr;
+  long long sh_send_cap = 0, sh_recv_cap = 0, sh_stage_cap = 0;
+  const double* sh_y = nullptr;  // this slice's local slab (device)
+  int sh_phase = 0;              // 0 idle, 1 mode-s input gather, 2 growth-mode input gather
+  int sh_em = -1, sh_header = 0;
+  long long sh_count = 0;
+  std::chrono::steady_clock::time_point sh_t0;
+
+  void shard_setup(int rank, int world, const long long* bounds) {
+    if (!initialized) fail(TSG_EINVAL, "shard_setup: state not initialised");
+    if (world < 1 || world > kMaxShards || rank < 0 || rank >= world)
+      fail(TSG_EINVAL, "shard_setup: bad rank / world size");
+    const long long ns = N[d - 2];
+    if (bounds[0] != 0 || bounds[world] != ns)
+      fail(TSG_EINVAL, "shard_setup: bounds must cover [0, N_s) of the last spatial mode");
+    for (int g = 0; g < world; ++g)
+      if (bounds[g + 1] <= bounds[g]) fail(TSG_EINVAL, "shard_setup: every rank needs >= 1 row");
+    flush();
+    shard_world = world;
+    shard_rank = rank;
+    for (int g = 0; g < world; ++g) {
+      shard_lo[g] = bounds[g];
+      shard_n[g] = bounds[g + 1] - bounds[g];
+    }
+    if (!sh_z) sh_z = dalloc(slice_elems);
+  }
+  long long shard_max_n() const {
+    long long m = 0;
+    for (int g = 0; g < shard_world; ++g) m = std::max(m, shard_n[g]);
+    return m;
+  }
+  void shard_buffers(long long count) {
+    if (count > sh_send_cap) {
+      dfree(sh_send);
+      sh_send = dalloc(count);
+      sh_send_cap = count;
+    }
+    if (count * shard_world > sh_recv_cap) {
+      dfree(sh_recv);
+      sh_recv = dalloc(count * shard_world);
+      sh_recv_cap = count * shard_world;
+    }
+  }
+  // Project the local slab through modes [0, m_end); the last output (the
+  // slab itself when m_end == 0) lands in sh_send + header, the per-mode
+  // partial pairs (when header > 0) in sh_send[0, 2 m_end).
+  void shard_local_pass(int m_end, int header) {
+    long long yd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+    yd[d - 2] = shard_n[shard_rank];
+    ShardPairs sp;
+    std::memset(&sp, 0, sizeof sp);
+    sp.partial = partial;
+    sp.nmodes = m_end;
+    const double* cur = sh_y;
+    int off = 0;
+    for (int k = 0; k < m_end; ++k) {
+      double* out = (k == m_end - 1) ? sh_send + header : pick(cur, nullptr);
+      sp.off[k] = off;
+      sp.cnt[k] = project(cur, yd, k, out, partial + off);
+      off += 2 * sp.cnt[k];
+      yd[k] = R[k];
+      cur = out;
+    }
+    if (m_end == 0)
+      ck(cudaMemcpyAsync(sh_send + header, sh_y, sizeof(double) * prod(yd, d - 1),
+                         cudaMemcpyDeviceToDevice, st), "slab copy");
+    if (header > 0) launch_shard_pack_pairs(sp, sh_send, st);
+  }
+  void shard_request(tsg_exchange* ex) {
+    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    ck(cudaGetLastError(), "shard local pass");
+    ex->pending = 1;
+    ex->count = sh_count;
+    ex->send = sh_send;
+    ex->recv = sh_recv;
+  }
+  void shard_done(tsg_exchange* ex) {
+    sh_phase = 0;
+    sync();
+    drain(true);
+    pull_ctrl();
+    r_exact = ctrl_h->r;
+    ex->pending = 0;
+    ex->count = 0;
+    ex->send = ex->recv = nullptr;
+    check_status();
+  }
+
+  void shard_begin(const double* slab, int mem_kind, tsg_exchange* ex) {
+    if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
+    if (shard_world == 0) fail(TSG_EINVAL, "tsg_shard_begin: call tsg_shard_setup first");
+    if (sh_phase != 0) fail(TSG_EINVAL, "tsg_shard_begin: the previous slice's exchange is pending");
+    flush();
+    sh_t0 = std::chrono::steady_clock::now();
+    const int s = d - 2;
+    const long long le = prod(N, s) * shard_n[shard_rank];
+    const bool misaligned = (reinterpret_cast<uintptr_t>(slab) & 15) != 0;
+    if (mem_kind == TSG_MEM_HOST || misaligned) {
+      if (le > sh_stage_cap) {
+        dfree(sh_stage);
+        sh_stage = dalloc(le);
+        sh_stage_cap = le;
+      }
+      ck(cudaMemcpyAsync(sh_stage, slab, sizeof(double) * le,
+                         mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                         st), "slab copy");
+      sh_y = sh_stage;
+    } else {
+      sh_y = slab;
+    }
+    sh_header = 2 * s;
+    sh_count = (sh_header + prod(R, s) * shard_max_n() + 1) / 2 * 2;
+    shard_buffers(sh_count);
+    shard_local_pass(s, sh_header);
+    sh_phase = 1;
+    shard_request(ex);
+  }
+
+  void shard_continue(tsg_exchange* ex) {
+    if (sh_phase == 0) fail(TSG_EINVAL, "tsg_shard_continue: no exchange pending");
+    const int s = d - 2, G = shard_world;
+    ShardLayout L;
+    std::memset(&L, 0, sizeof L);
+    L.world = G;
+    L.count = sh_count;
+    for (int g = 0; g < G; ++g) {
+      L.lo[g] = shard_lo[g];
+      L.nloc[g] = shard_n[g];
+    }
+    long long yd[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
+    if (sh_phase == 2) {
+      // the gathered input of the growing mode: grow redundantly from it
+      const int em = sh_em;
+      L.header = 0;
+      L.inner = prod(R, em) * prod(N + em, s - em);
+      launch_shard_unpack(L, sh_recv, sh_z, nullptr, st);
+      for (int k = 0; k < em; ++k) yd[k] = R[k];
+      pull_ctrl();
+      run_growth(sh_z, yd, em, em, slots_h[0].delta, 0, sh_t0);
+      shard_done(ex);
+      return;
+    }
+    // phase 1: assemble the input of mode s and the per-rank pairs of the
+    // local modes (into the decision's partial area, rank order)
+    L.header = sh_header;
+    L.inner = prod(R, s);
+    launch_shard_unpack(L, sh_recv, sh_z, partial, st);
+    for (int k = 0; k < s; ++k) yd[k] = R[k];
+    DecideArgs da;
+    std::memset(&da, 0, sizeof da);
+    da.slot = slots;
+    da.nmodes = d - 1;
+    da.tau = tau;
+    da.order = d;
+    da.partial = partial;
+    da.first_mode = 0;
+    int off = 2 * G * s;
+    for (int k = 0; k < s; ++k) {
+      da.off[k] = 2 * G * k;
+      da.cnt[k] = G;
+    }
+    long long ydk[kMaxD];
+    std::memcpy(ydk, yd, sizeof yd);
+    const double* cur = sh_z;
+    for (int k = s; k + 1 < d; ++k) {
+      double* out = pick(cur, sh_z);
+      da.off[k] = off;
+      da.cnt[k] = project(cur, ydk, k, out, partial + off);
+      off += 2 * da.cnt[k];
+      ydk[k] = R[k];
+      cur = out;
+    }
+    launch_decide(da, st);
+    pull_slot(0);
+    const SliceCtl sc = slots_h[0];
+    if (sc.zero_slice) {
+      zero_slice_path(0, sh_t0);
+    } else if (sc.expand_mode < 0) {
+      enqueue_isvd(cur, 0, 0, st, true, sh_t0);
+    } else if (sc.expand_mode >= s) {
+      pull_ctrl();
+      run_growth(sh_z, yd, s, sc.expand_mode, sc.delta, 0, sh_t0);
+    } else {
+      // growth at a local mode: gather that mode's input, grow redundantly
+      sh_em = sc.expand_mode;
+      sh_count = (prod(R, sh_em) * prod(N + sh_em, s - sh_em) * shard_max_n() + 1) / 2 * 2;
+      shard_buffers(sh_count);
+      shard_local_pass(sh_em, 0);
+      sh_phase = 2;
+      shard_request(ex);
+      return;
+    }
+    shard_done(ex);
   }
 
   void flush() {
@@ -1269,6 +1501,10 @@ struct tsg_stream {
       upad_R[k] = 0;
     }
     stage[0] = stage[1] = nullptr;
+    sh_send = sh_recv = sh_z = sh_stage = nullptr;
+    sh_send_cap = sh_recv_cap = sh_stage_cap = 0;
+    shard_world = 0;
+    sh_phase = 0;
     have_prev = false;
     partial_cap = ipart_cap = 0;
     evec_n = 0;
@@ -1624,6 +1860,33 @@ int tsg_init(tsg_stream* h, const double* x, int32_t order, const int64_t* dims,
 
 int tsg_update(tsg_stream* h, const double* slice, int32_t mem_kind) {
   return guarded(h, [&] { h->update(slice, mem_kind); });
+}
+
+int tsg_shard_setup(tsg_stream* h, int32_t rank, int32_t world, const int64_t* bounds) {
+  return guarded(h, [&] {
+    if (!bounds) fail(TSG_EINVAL, "tsg_shard_setup: bounds must not be null");
+    if (world < 1 || world > kMaxShards) fail(TSG_EINVAL, "tsg_shard_setup: bad world size");
+    std::vector<long long> b(bounds, bounds + world + 1);
+    h->shard_setup(rank, world, b.data());
+  });
+}
+
+int tsg_shard_begin(tsg_stream* h, const double* slab, int32_t mem_kind, tsg_exchange* ex) {
+  const int rc = guarded(h, [&] {
+    if (!ex) fail(TSG_EINVAL, "tsg_shard_begin: exchange descriptor must not be null");
+    h->shard_begin(slab, mem_kind, ex);
+  });
+  if (rc != TSG_OK) h->sh_phase = 0;  // a failed slice leaves no exchange pending
+  return rc;
+}
+
+int tsg_shard_continue(tsg_stream* h, tsg_exchange* ex) {
+  const int rc = guarded(h, [&] {
+    if (!ex) fail(TSG_EINVAL, "tsg_shard_continue: exchange descriptor must not be null");
+    h->shard_continue(ex);
+  });
+  if (rc != TSG_OK) h->sh_phase = 0;  // a failed slice leaves no exchange pending
+  return rc;
 }
 
 int tsg_synchronize(tsg_stream* h) {

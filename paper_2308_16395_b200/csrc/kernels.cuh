@@ -182,4 +182,27 @@ void launch_coupling_check(Ctrl* ctrl, const double* core, const double* q,
 
 int measure_fp64_peaks(int device, double* dmma_tflops, double* dfma_tflops);
 
+// ------------------------------------------------------ sharded update
+constexpr int kMaxShards = 64;
+// Partial pairs of the locally projected modes (layout as in DecideArgs).
+struct ShardPairs {
+  const double* partial;
+  int off[kMaxD], cnt[kMaxD];
+  int nmodes;
+};
+// out[2k], out[2k+1] = (sum res_sq, sum x_sq) of mode k, fixed order.
+void launch_shard_pack_pairs(const ShardPairs& p, double* out, cudaStream_t st);
+// Gathered buffer: rank g's block starts at g * count and holds `header`
+// doubles of pairs, then inner * nloc[g] doubles of its chunk, which lands
+// at z + inner * lo[g]. pairs_out (may be null) receives the pairs grouped
+// per mode: [k * 2 * world + 2 g + j].
+struct ShardLayout {
+  int world;
+  int header;
+  long long count, inner;
+  long long lo[kMaxShards], nloc[kMaxShards];
+};
+void launch_shard_unpack(const ShardLayout& L, const double* recv, double* z, double* pairs_out,
+                         cudaStream_t st);
+
 }  // namespace tsg

@@ -77,6 +77,12 @@ class TsgDims(C.Structure):
     ]
 
 
+class TsgExchange(C.Structure):
+    """tsg_exchange (include/tsg.h): one allgather request of a sharded update."""
+    _fields_ = [("pending", C.c_int32), ("count", C.c_int64), ("send", C.c_void_p),
+                ("recv", C.c_void_p)]
+
+
 class TsgMetrics(C.Structure):
     _fields_ = [
         ("slice_index", C.c_int64), ("ranks", C.c_int64 * MAXD),
@@ -94,6 +100,7 @@ EXPORTED = [
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
     "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
+    "tsg_shard_setup", "tsg_shard_begin", "tsg_shard_continue",
 ]
 
 _LIB = None
@@ -143,6 +150,9 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.tsg_measure_fp64_peaks.argtypes = [C.c_int32, _dp, _dp]
     L.tsg_readback_bytes_per_update.argtypes = []
     L.tsg_readback_bytes_per_update.restype = C.c_int64
+    L.tsg_shard_setup.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _i64p]
+    L.tsg_shard_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TsgExchange)]
+    L.tsg_shard_continue.argtypes = [C.c_void_p, C.POINTER(TsgExchange)]
     _LIB = L
     return L
 

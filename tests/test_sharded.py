@@ -1,0 +1,276 @@
+"""Sharded streamed update (paper_2308_16395_b200/sharded.py).
+
+CPU (gloo, world size 2): the per-slice exchange protocol of include/tsg.h
+driven by `sharded.drive` over `TorchComm`, with a host stand-in engine whose
+payload is the raw slab and whose finish is the CPU checker on the gathered
+slice; the result must be bit-identical to the checker's unsharded run. Plus
+the decomposition identity the device engine relies on: projecting modes
+< s slab by slab and concatenating along s equals projecting the whole slice.
+
+GPU: the device engine (libtsg.so) over `LoopbackGroup` (G virtual ranks on
+one B200, exchange = device copy): every rank ends bitwise identical, and the
+state matches the reference's golden fixtures within the parity tolerances;
+and G = 1 through a real NCCL process group (the transport the multi-GPU
+bench uses)."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import cases
+import parity as P
+
+torch = pytest.importorskip("torch")
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+# ------------------------------------------------------------------- CPU
+def test_shard_bounds_and_slabs():
+    from paper_2308_16395_b200 import sharded as SH
+    assert SH.shard_bounds(10, 3) == [0, 4, 7, 10]
+    assert SH.shard_bounds(8, 8) == list(range(9))
+    with pytest.raises(ValueError):
+        SH.shard_bounds(3, 4)
+    dims = (4, 5, 6)
+    y = np.arange(np.prod(dims), dtype=np.float64)
+    b = SH.shard_bounds(dims[-1], 4)
+    parts = [SH.slab_of(y, dims, b, g) for g in range(4)]
+    np.testing.assert_array_equal(np.concatenate(parts), y)
+    t = y.reshape(dims[::-1]).transpose()  # t[i0, i1, i2]
+    np.testing.assert_array_equal(parts[1].reshape(6 * 0 + b[2] - b[1], 5, 4).transpose(),
+                                  t[:, :, b[1]:b[2]])
+
+
+def test_local_projection_then_gather_equals_full():
+    """Modes < s are local to a slab of the last spatial mode: project each
+    slab, concatenate along s == project the slice (streaming.cpp:126-133)."""
+    g = np.random.default_rng(5)
+    dims = (7, 6, 9)
+    y = g.standard_normal(dims)
+    us = [np.linalg.qr(g.standard_normal((n, r)))[0] for n, r in zip(dims[:2], (3, 2))]
+
+    def proj(t):
+        res = []
+        for k, u in enumerate(us):
+            p = np.moveaxis(np.tensordot(u.T, t, axes=([1], [k])), 0, k)
+            res.append(np.linalg.norm(t - np.moveaxis(np.tensordot(u, p, axes=([1], [k])), 0, k)) ** 2)
+            t = p
+        return t, res
+
+    full, rfull = proj(y)
+    bounds = [0, 3, 5, 9]
+    pieces = [proj(y[:, :, bounds[i]:bounds[i + 1]]) for i in range(3)]
+    np.testing.assert_allclose(np.concatenate([p[0] for p in pieces], axis=2), full, rtol=1e-13, atol=1e-14)
+    for k in range(2):
+        np.testing.assert_allclose(sum(p[1][k] for p in pieces), rfull[k], rtol=1e-12)
+
+
+class _HostEngine:
+    """Host stand-in for the device engine with the same protocol surface
+    (begin / exchange_tensors / cont): the payload is the raw slab, the finish
+    runs the CPU checker on the gathered slice."""
+
+    class Ex:
+        def __init__(self, pending, count):
+            self.pending, self.count = pending, count
+
+    def __init__(self, handle, dims, bounds, rank, world):
+        self.h, self.dims, self.bounds, self.rank, self.world = handle, dims, bounds, rank, world
+        inner = int(np.prod(dims[:-1]))
+        self.inner = inner
+        self.count = inner * max(bounds[g + 1] - bounds[g] for g in range(world))
+        self.send = torch.zeros(self.count, dtype=torch.float64)
+        self.recv = torch.zeros(self.count * world, dtype=torch.float64)
+
+    def begin(self, slab):
+        self.send.zero_()
+        self.send[: len(slab)] = torch.from_numpy(np.asarray(slab))
+        return self.Ex(1, self.count)
+
+    def exchange_tensors(self, ex):
+        return self.send, self.recv
+
+    def cont(self, ex):
+        r = self.recv.numpy().reshape(self.world, self.count)
+        y = np.concatenate([r[g, : self.inner * (self.bounds[g + 1] - self.bounds[g])]
+                            for g in range(self.world)])
+        self.h.update_flat(y)
+        return self.Ex(0, 0)
+
+
+def _gloo_worker(rank, world, port, out_dir):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    sys.path.insert(0, os.path.join(root, "oracle"))
+    import torch.distributed as dist
+    from paper_2308_16395_b200 import datagen as dg, sharded as SH
+    import py_oracle
+
+    dist.init_process_group("gloo")
+    comm = SH.TorchComm()
+    cfg = dg.scaled(dg.CONFIGS["c2"], (12, 10, 9), n_slices=9, n_init=3)
+    gen = dg.TuckerStream(cfg)
+    chk = py_oracle.load_oracle()
+    x = gen.init_numpy().reshape(gen.init_dims()[::-1]).transpose()
+    h = chk.stream_init(x, cfg.tau)
+    dims = cfg.slice_dims
+    bounds = SH.shard_bounds(dims[-1], world)
+    eng = _HostEngine(h, dims, bounds, rank, world)
+    ex_total = 0
+    for t in range(cfg.n_init, cfg.n_slices):
+        y = gen.slice_numpy(t)
+        n, _ = SH.drive(eng, SH.slab_of(y, dims, bounds, rank), comm)
+        ex_total += n
+    st = h.export()
+    rec = {"rank": rank, "exchanges": ex_total, "core": [float(v) for v in np.ravel(st.core)],
+           "n_d": int(st.n_d), "err": float(st.squared_error)}
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(rec, f)
+    dist.destroy_process_group()
+
+
+def test_two_gloo_ranks_sharded_protocol(tmp_path, oracle):
+    import torch.multiprocessing as mp
+    from paper_2308_16395_b200 import datagen as dg
+    world = 2
+    mp.spawn(_gloo_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    recs = [json.load(open(tmp_path / f"rank{r}.json")) for r in range(world)]
+    cfg = dg.scaled(dg.CONFIGS["c2"], (12, 10, 9), n_slices=9, n_init=3)
+    gen = dg.TuckerStream(cfg)
+    h = oracle.stream_init(gen.init_numpy().reshape(gen.init_dims()[::-1]).transpose(), cfg.tau)
+    for t in range(cfg.n_init, cfg.n_slices):
+        h.update_flat(gen.slice_numpy(t))
+    ref = h.export()
+    for r in recs:
+        assert r["exchanges"] == cfg.n_slices - cfg.n_init      # one allgather per slice
+        assert r["n_d"] == ref.n_d
+        assert r["core"] == [float(v) for v in np.ravel(ref.core)]  # bitwise
+    assert recs[0]["core"] == recs[1]["core"]
+
+
+# ------------------------------------------------------------------- GPU
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _run_loopback(case, world, bounds=None):
+    from paper_2308_16395_b200 import sharded as SH
+    states = []
+    for g in range(world):
+        st = SH.ShardedStreamingState(device=0)
+        st.init_flat(case.init_flat, case.init_dims, case.tau)
+        b = st.setup(g, world, bounds)
+        states.append(st)
+    grp = SH.LoopbackGroup(states)
+    dims = tuple(case.init_dims[:-1])
+    for y in case.slices:
+        grp.stream_update([np.ascontiguousarray(SH.slab_of(y, dims, b, g)) for g in range(world)])
+    return states
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,world", [("c1", 2), ("c1", 3), ("growth24", 2), ("growth24", 4),
+                                        ("c3_40", 2), ("order5", 2), ("edges", 2), ("order2", 2),
+                                        ("thin", 2), ("random_full", 3)])
+def test_loopback_sharded_vs_golden(golden, name, world):
+    _need_gpu()
+    case = cases.STREAM_CASES[name]()
+    if case.init_dims[-2] < world:
+        pytest.skip("fewer rows than ranks")
+    states = _run_loopback(case, world)
+    ex = [st.export() for st in states]
+    for other in ex[1:]:  # every rank bitwise identical
+        assert other.core_dims == ex[0].core_dims
+        np.testing.assert_array_equal(other.core, ex[0].core)
+        np.testing.assert_array_equal(other.left, ex[0].left)
+        np.testing.assert_array_equal(other.sigma, ex[0].sigma)
+        for a, b in zip(other.factors, ex[0].factors):
+            np.testing.assert_array_equal(a, b)
+        assert other.squared_error == ex[0].squared_error
+        assert other.nonstream_discarded_sq == ex[0].nonstream_discarded_sq
+    g = golden("stream_" + name)
+    mg = P.metrics_arrays(states[0].metrics(), ex[0].order)
+    mc = P.compare_metrics(mg, P.golden_metrics(g), float(g["total_input_sq"]))
+    sc = P.compare_states(ex[0], P.state_from_golden(g))
+    print(name, world, mc, sc)
+    P.assert_parity(mc, sc)
+
+
+@pytest.mark.gpu
+def test_sharded_uneven_bounds_and_errors(golden):
+    _need_gpu()
+    from paper_2308_16395_b200 import sharded as SH
+    from paper_2308_16395_b200 import streaming as S
+    case = cases.STREAM_CASES["growth24"]()
+    n = case.init_dims[-2]
+    states = _run_loopback(case, 3, bounds=[0, 1, n - 2, n])
+    g = golden("stream_growth24")
+    e = states[0].export()
+    mc = P.compare_metrics(P.metrics_arrays(states[0].metrics(), e.order), P.golden_metrics(g),
+                           float(g["total_input_sq"]))
+    P.assert_parity(mc, P.compare_states(e, P.state_from_golden(g)))
+    st = SH.ShardedStreamingState(device=0)
+    st.init_flat(case.init_flat, case.init_dims, case.tau)
+    with pytest.raises(S.InvalidArgument):
+        st.setup(0, 2, [0, 0, n])           # an empty shard
+    with pytest.raises(S.InvalidArgument):
+        st.setup(2, 2)                      # rank out of range
+    with pytest.raises(S.InvalidArgument):
+        st.begin(np.zeros(4))               # not set up
+    st.setup(0, 2)
+    with pytest.raises(S.InvalidArgument):
+        st.cont(S.TsgExchange())            # nothing pending
+
+
+def _nccl_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), WORLD_SIZE=str(world),
+                      RANK=str(rank), LOCAL_RANK=str(rank))
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    for p in (root, os.path.join(root, "tests"), os.path.join(root, "oracle")):
+        sys.path.insert(0, p)
+    import torch.distributed as dist
+    import cases as CS
+    from paper_2308_16395_b200 import sharded as SH
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl")
+    case = CS.STREAM_CASES["growth24"]()
+    st = SH.ShardedStreamingState(device=rank)
+    st.init_flat(case.init_flat, case.init_dims, case.tau)
+    b = st.setup(rank, world)
+    comm = SH.TorchComm()
+    dims = tuple(case.init_dims[:-1])
+    for y in case.slices:
+        st.stream_update_slab(np.ascontiguousarray(SH.slab_of(y, dims, b, rank)), comm)
+    e = st.export()
+    np.savez(q, core=e.core, left=e.left, sigma=e.sigma, exchanges=st.exchanges)
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_nccl_transport_world1_matches_loopback(tmp_path):
+    """The torch.distributed NCCL path (ExternalStream on the engine stream)
+    with one rank gives the same bytes as the loopback exchange."""
+    _need_gpu()
+    import torch.multiprocessing as mp
+    out = str(tmp_path / "r0.npz")
+    mp.spawn(_nccl_worker, args=(1, _free_port(), out), nprocs=1, join=True)
+    z = np.load(out)
+    case = cases.STREAM_CASES["growth24"]()
+    ref = _run_loopback(case, 1)[0].export()
+    np.testing.assert_array_equal(z["core"], ref.core)
+    np.testing.assert_array_equal(z["left"], ref.left)
+    assert int(z["exchanges"]) >= len(case.slices)
