@@ -12,8 +12,10 @@ Our arm: slices are synthesised on the device before the timed region and
 each step reads a distinct slice (never re-read), so no step hits L2 with
 its input. W untimed updates, then K timed updates bracketed by a barrier and
 synchronisation; time = CUDA events on the engine's stream, max over ranks.
-For N>1 every rank runs an independent replica stream (replicas only; the
-sharded mode of SURVEY §8(e) is not built yet) and value = total slices/s.
+For N>1 (torchrun) the default is the sharded engine: one
+stream, each slice split along its last spatial mode over the GPUs, one NCCL
+allgather per slice, "scaling": "strong"; --mode replicas runs independent
+streams instead (weak scaling). value = slices/s of the whole job.
 """
 from __future__ import annotations
 
@@ -290,6 +292,90 @@ def run_ours(args, world, rank, local):
     return out
 
 
+# ----------------------------------------------------- sharded (N > 1)
+def run_sharded(args, world, rank, local):
+    """One stream split over `world` GPUs: every rank holds the
+    full state and rows [lo, hi) of the last spatial mode of each slice; one
+    NCCL allgather of the compressed local tensor per slice. Strong scaling:
+    the work per step (one slice) is fixed as N grows."""
+    import torch
+    from paper_2308_16395_b200 import datagen as dg
+    from paper_2308_16395_b200 import sharded as SH
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = dg.CONFIGS[args.config]
+    gen = dg.TuckerStream(cfg)  # the same stream on every rank
+    init = torch.cat([gen.slice_torch(t, dev) for t in range(cfg.n_init)])
+    st = SH.ShardedStreamingState(device=local)
+    st.init_flat(init, gen.init_dims(), cfg.tau)
+    del init
+    bounds = st.setup(rank, world)
+    dims = cfg.slice_dims
+    nsl = args.warmup + args.steps
+    slabs = [SH.slab_of(gen.slice_torch(cfg.n_init + i, dev), dims, bounds, rank).clone()
+             for i in range(nsl)]
+    torch.cuda.synchronize()
+    comm = SH.TorchComm() if world > 1 else _LocalComm()
+    for i in range(args.warmup):
+        st.stream_update_slab(slabs[i], comm)
+    launches0 = st.kernel_launches()
+    ex0, xd0 = st.exchanges, st.exchanged_doubles
+    ext = torch.cuda.ExternalStream(st.cuda_stream(), device=dev)
+    clocks = ClockSampler(local)
+    barrier(world)
+    torch.cuda.synchronize()
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(ext)
+    for i in range(args.warmup, nsl):
+        st.stream_update_slab(slabs[i], comm)
+    e1.record(ext)
+    e1.synchronize()
+    torch.cuda.synchronize()
+    barrier(world)
+    clk = clocks.stop()
+    ms = allreduce_max(world, e0.elapsed_time(e1))
+    q = st.query()
+    value = args.steps / (ms / 1e3)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "gbs_ingested": value * cfg.slice_bytes / 1e9,
+        "config": {"workload": f"{args.config}: {cfg.notes}", "slice_dims": list(dims),
+                   "tau": cfg.tau, "eta": cfg.eta, "n_init": cfg.n_init,
+                   "ranks_after": list(q["core_dims"]), "n_d_after": q["n_d"],
+                   "parallelism": f"sharded{world} (last spatial mode, rows {bounds})",
+                   "l2": "each step reads a distinct device-resident slab (never re-read)",
+                   "mode": "sharded engine: local modes, one allgather per slice, redundant finish"},
+        "exchange": {"allgathers_per_step": (st.exchanges - ex0) / args.steps,
+                     "bytes_gathered_per_rank_per_step":
+                         8.0 * (st.exchanged_doubles - xd0) / args.steps / world},
+        "clocks": clk, "gpu_launches": st.kernel_launches() - launches0,
+        "e2e": None, "roofline": None, "cpu_baseline": None,
+    }
+    st.close()
+    return out
+
+
+class _LocalComm:
+    """World size 1 without a process group: the gather is a copy."""
+
+    def allgather(self, send, recv, stream=None):
+        import torch
+        with torch.cuda.stream(stream) if stream is not None else _null():
+            recv.copy_(send)
+
+
+class _null:
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        return False
+
+
 def load_traffic(config):
     p = os.path.join(ROOT, "profiles", f"traffic_{config}.json")
     if os.path.exists(p):
@@ -390,6 +476,9 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-slices", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="auto", choices=["auto", "sharded", "replicas", "single"],
+                    help="N>1: sharded (one stream split over the GPUs, default) or replicas "
+                         "(independent streams); N=1: single engine (default) or sharded")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -402,8 +491,9 @@ def main():
         print(json.dumps(run_reference(args, world, rank)))
         return
     world, rank, local = dist_setup(args)
-    if False:
-        pass
+    mode = args.mode if args.mode != "auto" else ("sharded" if world > 1 else "single")
+    if mode == "sharded":
+        out = run_sharded(args, world, rank, local)
     else:
         out = run_ours(args, world, rank, local)
     if rank == 0:
