@@ -154,7 +154,9 @@ __global__ void pad_u_kernel(const double* __restrict__ u, long long N, int R, i
        idx += (long long)gridDim.x * blockDim.x) {
     const long long row = idx / rpad;
     const int col = (int)(idx % rpad);
-    out[idx] = (row < N && col < R) ? u[row + col * N] : 0.0;
+    // image column 8rt + 2t + i holds rank 8rt + 4i + t (see proj_dmma.cuh)
+    const int rk = (col & ~7) + 4 * (col & 1) + ((col & 7) >> 1);
+    out[idx] = (row < N && col < (rpad & ~7) && rk < R) ? u[row + rk * N] : 0.0;
   }
 }
 

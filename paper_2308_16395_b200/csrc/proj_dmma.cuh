@@ -10,8 +10,10 @@
 // The K index inside phase 1 is permuted (k-step (grp, i), lane t -> row
 // 8 grp + 2t + i) so that the A fragments a thread feeds phase 1 are exactly
 // the X elements its phase-2 accumulators cover, and phase 2's K index is
-// permuted (k-step (rt, i), lane t -> rank 8 rt + 2t + i) so its A fragments
-// are exactly the thread's reduced phase-1 accumulators. X therefore lives in
+// permuted (k-step (rt, i), lane t -> rank 8 rt + 4i + t; the U image holds
+// rank 8rt + 4i + t in column 8rt + 2t + i) so its A fragments are exactly
+// the thread's reduced phase-1 accumulators and a K-step of ranks >= R
+// (R - 8(RT-1) <= 4: the last tile's i = 1 step) is skipped. X therefore lives in
 // registers only (read once from HBM, prefetched one tile ahead), U is staged
 // once per CTA in shared memory with a conflict-minimal row pitch (8 RT + 4).
 // Reference: streaming.cpp:128-133 (ttm pair + residual), tensor.cpp:106-162.
@@ -28,6 +30,14 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
+}
+
+// Same instruction without `volatile`, so the compiler may interleave
+// independent accumulator chains (the result is always consumed).
+__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
 }
 
 template <int RT, int MC, int NW = 8>
@@ -206,7 +216,8 @@ __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb
 #pragma unroll 4
     for (int idx = threadIdx.x; idx < total; idx += blockDim.x) {
       const int col = idx / rows8, row = idx - col * rows8;
-      Us[row * RPAD + col] = (row < N && col < R) ? __ldg(a.u + row + (long long)col * N) : 0.0;
+      const int rk = (col & ~7) + 4 * (col & 1) + ((col & 7) >> 1);
+      Us[row * RPAD + col] = (row < N && col < 8 * RT && rk < R) ? __ldg(a.u + row + (long long)rk * N) : 0.0;
     }
   }
   __syncthreads();
@@ -300,7 +311,7 @@ __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb
             if (((mc * RT + rt) % NW) != warp) continue;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-              const int j = 8 * rt + 2 * t + i;
+              const int j = 8 * rt + 4 * i + t;
               if (j < R) pout[(long long)j * left] = acc[mc][rt][i];
             }
           }
@@ -419,7 +430,7 @@ inline int launch_t(const ProjArgs& a, int streaming_in, cudaStream_t st) {
 // per tile and an mbarrier per stage, keeping ~(NS-1) tiles in flight per SM
 // (load latency, not bandwidth, limited the register-prefetch path). The
 // math is the same two-phase DMMA scheme as proj_dmma_kernel.
-template <int RT, int MC, int GM, bool WE, int MINB = 1>
+template <int RT, int MC, int GM, bool WE, int MINB = 1, bool HALF = false>
 __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
   const int NS = a.karg0;
   extern __shared__ __align__(128) unsigned char smraw[];
@@ -436,6 +447,7 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
   unsigned long long* bar = reinterpret_cast<unsigned long long*>(red + 9 * PER * 32);
   unsigned long long* ubar = bar + NS;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const bool last_ok = warp + 8 * (GM - 1) < ngroups;  // warp-uniform
   const int g = lane >> 2, t = lane & 3;
   const long long ntiles = (cols + BN - 1) / BN;
   const double* xsrc = a.x;
@@ -495,23 +507,25 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
     for (int mc = 0; mc < MC; ++mc)
 #pragma unroll
       for (int rt = 0; rt < RT; ++rt) acc[mc][rt][0] = acc[mc][rt][1] = 0.0;
-#pragma unroll
-    for (int gi = 0; gi < GM; ++gi) {
+    // slots gi < GM-1 always hold a row group; the last one only for some
+    // warps (a real branch, so no predicated-off DMMA occupies the pipe)
+    auto p1 = [&](int gi) {
       const int grp = warp + 8 * gi;
-      if (grp < ngroups) {
 #pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const double* urow = Us + (8 * grp + 2 * t + i) * RPAD + g;
-          double b[RT];
+      for (int i = 0; i < 2; ++i) {
+        const double* urow = Us + (8 * grp + 2 * t + i) * RPAD + g;
+        double b[RT];
 #pragma unroll
-          for (int rt = 0; rt < RT; ++rt) b[rt] = urow[8 * rt];
+        for (int rt = 0; rt < RT; ++rt) b[rt] = urow[8 * rt];
 #pragma unroll
-          for (int mc = 0; mc < MC; ++mc)
+        for (int mc = 0; mc < MC; ++mc)
 #pragma unroll
-            for (int rt = 0; rt < RT; ++rt) dmma(acc[mc][rt][0], acc[mc][rt][1], X[mc][gi][i], b[rt]);
-        }
+          for (int rt = 0; rt < RT; ++rt) dmma(acc[mc][rt][0], acc[mc][rt][1], X[mc][gi][i], b[rt]);
       }
-    }
+    };
+#pragma unroll
+    for (int gi = 0; gi + 1 < GM; ++gi) p1(gi);
+    if (last_ok) p1(GM - 1);
     // ---- cross-warp reduction (reduce-scatter then gather; fixed order)
     double* myred = red + warp * (PER * 32);
 #pragma unroll
@@ -546,7 +560,7 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
             if (((mc * RT + rt) & 7) != warp) continue;
 #pragma unroll
             for (int i = 0; i < 2; ++i) {
-              const int j = 8 * rt + 2 * t + i;
+              const int j = 8 * rt + 4 * i + t;
               if (j < R) a.p[c * R + j] = acc[mc][rt][i];
             }
           }
@@ -560,19 +574,29 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
       for (int gi = 0; gi < GM; ++gi)
 #pragma unroll
         for (int mc = 0; mc < MC; ++mc) c2[gi][mc][0] = c2[gi][mc][1] = 0.0;
+      auto p2 = [&](int gi, int rt, int i) {
+        const int grp = warp + 8 * gi;
+        const double b = Us[(8 * grp + g) * RPAD + 2 * t + 8 * rt + i];
+#pragma unroll
+        for (int mc = 0; mc < MC; ++mc) dmma(c2[gi][mc][0], c2[gi][mc][1], acc[mc][rt][i], b);
+      };
+      // K-step (rt, i) = ranks 8rt + 4i .. +3: the last tile's second step is
+      // all padding when HALF
 #pragma unroll
       for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
         for (int i = 0; i < 2; ++i)
+          if (!(HALF && rt == RT - 1 && i == 1)) {
 #pragma unroll
-          for (int gi = 0; gi < GM; ++gi) {
-            const int grp = warp + 8 * gi;
-            if (grp < ngroups) {
-              const double b = Us[(8 * grp + g) * RPAD + 2 * t + 8 * rt + i];
-#pragma unroll
-              for (int mc = 0; mc < MC; ++mc) dmma(c2[gi][mc][0], c2[gi][mc][1], acc[mc][rt][i], b);
-            }
+            for (int gi = 0; gi + 1 < GM; ++gi) p2(gi, rt, i);
           }
+      if (last_ok) {
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+            if (!(HALF && rt == RT - 1 && i == 1)) p2(GM - 1, rt, i);
+      }
 #pragma unroll
       for (int gi = 0; gi < GM; ++gi) {
         const int grp = warp + 8 * gi;
@@ -618,8 +642,8 @@ inline size_t smem0_bytes(int RT, int MC, long long N, int NS) {
          (NS + 1) * sizeof(unsigned long long);
 }
 
-template <int RT, int MC, int GM, bool WE, int MINB>
-inline int launch0_t(const ProjArgs& a, cudaStream_t st) {
+template <int RT, int MC, int GM, bool WE, int MINB, bool HALF>
+inline int launch0_th(const ProjArgs& a, cudaStream_t st) {
   const size_t cap = MINB == 1 ? 225 * 1024 : 111 * 1024;
   int NS = 8;
   while (NS >= 3 && smem0_bytes(RT, MC, a.v.n, NS) > cap) --NS;
@@ -627,7 +651,7 @@ inline int launch0_t(const ProjArgs& a, cudaStream_t st) {
   const size_t smem = smem0_bytes(RT, MC, a.v.n, NS);
   static size_t attr = 0;
   if (smem > attr) {
-    if (cudaFuncSetAttribute(proj0_tma_kernel<RT, MC, GM, WE, MINB>,
+    if (cudaFuncSetAttribute(proj0_tma_kernel<RT, MC, GM, WE, MINB, HALF>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap) != cudaSuccess)
       return -1;
     attr = cap;
@@ -644,8 +668,14 @@ inline int launch0_t(const ProjArgs& a, cudaStream_t st) {
   const int grid = (int)(ntiles < slots ? (ntiles < 1 ? 1 : ntiles) : slots);
   ProjArgs b = a;
   b.karg0 = NS;
-  proj0_tma_kernel<RT, MC, GM, WE, MINB><<<grid, 256, smem, st>>>(b);
+  proj0_tma_kernel<RT, MC, GM, WE, MINB, HALF><<<grid, 256, smem, st>>>(b);
   return grid;
+}
+
+template <int RT, int MC, int GM, bool WE, int MINB>
+inline int launch0_t(const ProjArgs& a, cudaStream_t st) {
+  return (a.R - 8 * (RT - 1) <= 4) ? launch0_th<RT, MC, GM, WE, MINB, true>(a, st)
+                                   : launch0_th<RT, MC, GM, WE, MINB, false>(a, st);
 }
 
 template <int RT, int MC, int GM>
@@ -661,10 +691,290 @@ inline int launch0_rt(const ProjArgs& a, cudaStream_t st) {
   return a.e ? launch0_t<RT, MC, GM, true, 1>(a, st) : launch0_t<RT, MC, GM, false, 1>(a, st);
 }
 
+// ---------------------------------------------------------------------------
+// Mode-0 projection, warp-owned column tiles ("proj0w"). Each of the 4 warps
+// of a CTA (one per SM sub-partition, one CTA per SM) streams its own 8-column
+// tiles (8 x N doubles, contiguous) through a private NS-stage ring filled by
+// one bulk copy (TMA) per tile and an mbarrier per stage, so no CTA-wide
+// barrier exists in the steady state and the whole fibre is in one warp:
+//   phase 1  P^T (8 x R) = X^T U over all N rows (K = N), two accumulator
+//            chains per rank tile (even / odd row octets) -> no cross-warp sum;
+//   phase 2  Rec^T (8 x N) = P^T U^T with K = R rounded up to 4 (not 8): the
+//            rank columns are permuted (image column 8rt + 2t + i holds rank
+//            8rt + 4i + t) so a phase-1 accumulator pair covers two K-steps of
+//            four consecutive ranks and K-steps beyond R are skipped;
+//   epilogue E = X - Rec from the staged tile, ||E||^2, ||X||^2 (and E).
+// U is staged once per CTA, row-major with pitch 8 RT + 4 (conflict-free
+// fragment loads). DMMA per 8 columns: N/4 RT + (N/8) ceil(R/4).
+template <int RT, int KS, bool WE>
+__global__ void __launch_bounds__(128, 1) proj0w_kernel(ProjArgs a) {
+  constexpr int RP = 8 * RT + 4;  // phase-1 image pitch (row-major, permuted rank columns)
+  const int NS = a.karg0;
+  const int N = (int)a.v.n;  // even
+  const long long cols = a.v.right;
+  const int R = a.R;
+  const int ng = (N + 7) >> 3;   // row octets
+  const int N8 = ng * 8;
+  const int CP = N8 + 4;         // phase-2 image pitch (rank-major, rows contiguous)
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ double sred[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = lane >> 2, t = lane & 3;
+  double* Us = reinterpret_cast<double*>(smraw);                   // N8 x RP
+  double* Vs = Us + (long long)N8 * RP;                            // 4 KS x CP
+  double* ring = Vs + (long long)4 * KS * CP;                      // [4][NS][8 N8]
+  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ring + 4LL * NS * 8 * N8);
+  double* wring = ring + (long long)warp * NS * 8 * N8;
+  unsigned long long* wbar = bar + warp * NS;
+  const long long ntiles = (cols + 7) >> 3;
+  const long long stride = (long long)gridDim.x * 4;
+  const long long first = (long long)blockIdx.x * 4 + warp;
+  const double* xsrc = a.x;
+  auto issue = [&](long long tl, int s) {
+    const long long c0 = tl * 8;
+    const long long nc = (cols - c0) < 8 ? (cols - c0) : 8;
+    const unsigned bytes = (unsigned)(nc * N * 8);
+    mbar_expect_tx(&wbar[s], bytes);
+    bulk_g2s(wring + (long long)s * 8 * N8, xsrc + c0 * N, bytes, &wbar[s]);
+  };
+  // Rows N..N8-1 of the last column of a stage read the stage tail (zeroed
+  // once; the TMA never writes it) against zero U rows. Columns beyond a short
+  // last tile only feed their own (discarded) output rows.
+  if (N8 > N)
+    for (int i = threadIdx.x; i < 4 * NS * 8 * (N8 - N); i += 128) {
+      const int st_ = i / (8 * (N8 - N)), o = i - st_ * 8 * (N8 - N);
+      ring[(long long)st_ * 8 * N8 + 8 * N + o] = 0.0;
+    }
+  // phase-1 image: Us[row][8rt + 2t + i] = U[row][8rt + 4i + t]
+  for (int i = threadIdx.x; i < N8 * RP; i += 128) {
+    const int row = i / RP, c = i - row * RP;
+    const int rk = c < 8 * RT ? (c & ~7) + 4 * (c & 1) + ((c & 7) >> 1) : R;
+    Us[i] = (row < N && rk < R) ? __ldg(a.u + row + (long long)rk * N) : 0.0;
+  }
+  // phase-2 image: Vs[rank][row] (rank-major)
+  for (int i = threadIdx.x; i < 4 * KS * CP; i += 128) {
+    const int rk = i / CP, row = i - rk * CP;
+    Vs[i] = (row < N && rk < R) ? __ldg(a.u + row + (long long)rk * N) : 0.0;
+  }
+  if (threadIdx.x < 4 * NS) mbar_init(&bar[threadIdx.x], 1);
+  mbar_fence_init();
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+  if (lane == 0)
+    for (int s = 0; s < NS - 1; ++s) {
+      const long long tl = first + (long long)s * stride;
+      if (tl < ntiles) issue(tl, s);
+    }
+  double racc = 0.0, xacc = 0.0;
+  int it = 0;
+#pragma unroll 1
+  for (long long tile = first; tile < ntiles; tile += stride, ++it) {
+    const int s = it % NS;
+    if (lane == 0) {
+      const long long tl = tile + (long long)(NS - 1) * stride;
+      if (tl < ntiles) issue(tl, (it + NS - 1) % NS);
+    }
+    mbar_wait(&wbar[s], (unsigned)((it / NS) & 1));
+    const double* xt = wring + (long long)s * 8 * N8 + g * N;  // this lane's column
+    // ---- phase 1: two octets per step into two accumulator sets; dependent
+    // DMMAs sit 2 RT instructions apart (volatile asm keeps this order), the
+    // next step's operands are loaded before this step's DMMAs
+    const double* up = Us + (2 * t) * RP + g;
+    double acc[2][RT][2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+      for (int rt = 0; rt < RT; ++rt) acc[h][rt][0] = acc[h][rt][1] = 0.0;
+    struct Ops {
+      double2 xv[2];
+      double b0[2][RT], b1[2][RT];
+    };
+    auto load = [&](int q, Ops& o) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int qq = q + h < ng ? q + h : ng - 1;  // clamped (an odd tail feeds zeros below)
+        o.xv[h] = *reinterpret_cast<const double2*>(xt + 8 * qq + 2 * t);
+        const double* uq = up + (8 * qq) * RP;
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt) {
+          o.b0[h][rt] = uq[8 * rt];
+          o.b1[h][rt] = uq[RP + 8 * rt];
+        }
+      }
+    };
+    auto compute = [&](const Ops& o, int nh) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt)
+          dmma(acc[h][rt][0], acc[h][rt][1], h < nh ? o.xv[h].x : 0.0, o.b0[h][rt]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int rt = 0; rt < RT; ++rt)
+          dmma(acc[h][rt][0], acc[h][rt][1], h < nh ? o.xv[h].y : 0.0, o.b1[h][rt]);
+    };
+    {
+      Ops cur, nxt;
+      load(0, cur);
+      int q = 0;
+#pragma unroll 1
+      for (; q + 2 < ng; q += 2) {
+        load(q + 2, nxt);
+        compute(cur, 2);
+        cur = nxt;
+      }
+      compute(cur, ng - q);  // last one or two octets
+    }
+    double pv[RT][2];
+#pragma unroll
+    for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) pv[rt][i] = acc[0][rt][i] + acc[1][rt][i];
+    const long long c = tile * 8 + g;
+    const bool cv = c < cols;
+    if (a.p && cv) {
+#pragma unroll
+      for (int rt = 0; rt < RT; ++rt)
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const int j = 8 * rt + 4 * i + t;
+          if (j < R) a.p[c * R + j] = pv[rt][i];
+        }
+    }
+    // ---- phase 2 + epilogue, NB row octets at a time (NB independent chains
+    // of KS DMMAs); K-step k covers ranks 4k..4k+3 = accumulator pv[k/2][k%2]
+    if (a.residual) {
+      constexpr int NB = 4;
+      const double* vb = Vs + (long long)t * CP + g;  // Vs[4k + t][8 nt + g]
+      auto loadb = [&](int n0, double (&bv)[KS][NB]) {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int nt = n0 + j < ng ? n0 + j : ng - 1;
+#pragma unroll
+          for (int k = 0; k < KS; ++k) bv[k][j] = vb[(4 * k) * CP + 8 * nt];
+        }
+      };
+      auto block = [&](int n0, int nb, const double (&bv)[KS][NB]) {
+        double cc[NB][2];
+        double2 xv[NB];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          cc[j][0] = cc[j][1] = 0.0;
+          const int nt = n0 + j < ng ? n0 + j : ng - 1;
+          xv[j] = *reinterpret_cast<const double2*>(xt + 8 * nt + 2 * t);
+        }
+#pragma unroll
+        for (int k = 0; k < KS; ++k)
+#pragma unroll
+          for (int j = 0; j < NB; ++j) dmma(cc[j][0], cc[j][1], pv[k >> 1][k & 1], bv[k][j]);
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+          const int row = 8 * (n0 + j) + 2 * t;
+          if (j < nb && cv && row < N) {
+            const double e0 = xv[j].x - cc[j][0], e1 = xv[j].y - cc[j][1];
+            racc = fma(e0, e0, racc);
+            racc = fma(e1, e1, racc);
+            xacc = fma(xv[j].x, xv[j].x, xacc);
+            xacc = fma(xv[j].y, xv[j].y, xacc);
+            if constexpr (WE) {
+              a.e[c * N + row] = e0;
+              a.e[c * N + row + 1] = e1;
+            }
+          }
+        }
+      };
+      double bcur[KS][NB], bnxt[KS][NB];
+      loadb(0, bcur);
+      int n0 = 0;
+#pragma unroll 1
+      for (; n0 + NB < ng; n0 += NB) {
+        loadb(n0 + NB, bnxt);
+        block(n0, NB, bcur);
+#pragma unroll
+        for (int k = 0; k < KS; ++k)
+#pragma unroll
+          for (int j = 0; j < NB; ++j) bcur[k][j] = bnxt[k][j];
+      }
+      block(n0, ng - n0, bcur);
+    }
+    // the stage is refilled next iteration: every lane's reads are done
+    __syncwarp();
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
+  racc = block_sum(racc, sred);
+  xacc = block_sum(xacc, sred);
+  if (threadIdx.x == 0 && a.partial) {
+    a.partial[2 * blockIdx.x] = racc;
+    a.partial[2 * blockIdx.x + 1] = xacc;
+  }
+}
+
+template <int RT, int KS, bool WE>
+inline int launch0w_t(const ProjArgs& a, cudaStream_t st) {
+  const long long N = a.v.n;
+  const long long N8 = (N + 7) / 8 * 8;
+  const long long ubytes = N8 * (8 * RT + 4) * 8 + 4LL * KS * (N8 + 4) * 8;
+  const long long stage = 8 * N8 * 8;
+  const long long cap = 225 * 1024;
+  int NS = 4;
+  while (NS >= 2 && ubytes + 4 * NS * stage + 8 * 4 * NS > cap) --NS;
+  if (NS < 2) return -1;
+  const size_t smem = (size_t)(ubytes + 4 * NS * stage + 8 * 4 * NS);
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(proj0w_kernel<RT, KS, WE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)cap) != cudaSuccess)
+      return -1;
+    attr = cap;
+  }
+  const long long ntiles = (a.v.right + 7) / 8;
+  static const long long cap_ctas = [] {
+    const char* e = std::getenv("TSG_M0_CTAS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  long long grid = kNumSMs - 8;  // room for the overlapping tail / insertion kernels
+  if (cap_ctas > 0) grid = cap_ctas;
+  const long long need = (ntiles + 3) / 4;
+  if (need < grid) grid = need < 1 ? 1 : need;
+  ProjArgs b = a;
+  b.karg0 = NS;
+  proj0w_kernel<RT, KS, WE><<<(int)grid, 128, smem, st>>>(b);
+  return (int)grid;
+}
+
+template <int RT, int KS>
+inline int launch0w_k(const ProjArgs& a, cudaStream_t st) {
+  return a.e ? launch0w_t<RT, KS, true>(a, st) : launch0w_t<RT, KS, false>(a, st);
+}
+
+inline int launch0w(const ProjArgs& a, cudaStream_t st) {
+  static const int off = [] {  // opt-in (TSG_PROJ0W=1): one warp per SM sub-partition
+    const char* e = std::getenv("TSG_PROJ0W");
+    return e ? (std::atoi(e) == 0) : 1;
+  }();
+  if (off) return -1;
+  switch ((a.R + 3) / 4) {
+    case 1: return launch0w_k<1, 1>(a, st);
+    case 2: return launch0w_k<1, 2>(a, st);
+    case 3: return launch0w_k<2, 3>(a, st);
+    case 4: return launch0w_k<2, 4>(a, st);
+    case 5: return launch0w_k<3, 5>(a, st);
+    case 6: return launch0w_k<3, 6>(a, st);
+    case 7: return launch0w_k<4, 7>(a, st);
+    case 8: return launch0w_k<4, 8>(a, st);
+  }
+  return -1;
+}
+
 inline int launch0(const ProjArgs& a, cudaStream_t st) {
   const long long N = a.v.n;
   if (a.v.left != 1 || (N & 1) || N > 256 || a.R > 32 || a.R < 1 || !a.upad) return -1;
   if (a.v.right >= (1LL << 31)) return -1;
+  {
+    const int g = launch0w(a, st);
+    if (g > 0) return g;
+  }
   const int ngroups = (int)((N + 7) / 8);
   const int RT = (a.R + 7) / 8;
   if (ngroups <= 8) {
