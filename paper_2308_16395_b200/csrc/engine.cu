@@ -105,23 +105,26 @@ struct tsg_stream {
   cudaStream_t si = nullptr;
   cudaStream_t sc = nullptr;     // host-to-device copies (overlap with compute)
   cudaStream_t s2 = nullptr;     // trailing modes + decision (overlap the next mode 0)
-  cudaEvent_t ev_m0[2] = {nullptr, nullptr};
-  cudaEvent_t ev_h2d[2] = {nullptr, nullptr};
-  bool ev_h2d_valid[2] = {false, false};
-  SliceCtl* slots = nullptr;     // device [2]
-  SliceCtl* slots_h = nullptr;   // pinned mirror [2]
-  double* pw[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};
+  // kNP slices in flight: projections of slice t+1 and t+2 may run while the
+  // insertion of slice t does (per-slot buffers, decisions, events)
+  static constexpr int kNP = 3;
+  cudaEvent_t ev_m0[kNP] = {};
+  cudaEvent_t ev_h2d[kNP] = {};
+  bool ev_h2d_valid[kNP] = {};
+  SliceCtl* slots = nullptr;     // device [kNP]
+  SliceCtl* slots_h = nullptr;   // pinned mirror [kNP]
+  double* pw[kNP][2] = {};
   long long pipe_elems = 0;
-  cudaEvent_t ev_proj[2] = {nullptr, nullptr}, ev_isvd[2] = {nullptr, nullptr};
-  bool ev_isvd_valid[2] = {false, false};
+  cudaEvent_t ev_proj[kNP] = {}, ev_isvd[kNP] = {};
+  bool ev_isvd_valid[kNP] = {};
   long long upd_count = 0;
   // Host-mapped channels (no copy calls on the per-slice path): decisions
   // published by decide_kernel, the projection input pointer per parity, and
   // the per-insertion record ring.
-  SliceCtl* hslot = nullptr;              // mapped [2]
+  SliceCtl* hslot = nullptr;              // mapped [kNP]
   SliceCtl* hslot_d = nullptr;
-  unsigned long long* seq_dev = nullptr;  // device [2] decision counters
-  unsigned long long seq_expect[2] = {0, 0};
+  unsigned long long* seq_dev = nullptr;  // device [kNP] decision counters
+  unsigned long long seq_expect[kNP] = {};
   RecRing* ring_h = nullptr;              // mapped
   RecRing* ring_d = nullptr;
   unsigned long long rec_read = 0;        // records consumed by the host
@@ -190,7 +193,7 @@ struct tsg_stream {
     }
     auto it = graphs.find(key);
     if (it == graphs.end()) {
-      if (graphs.size() >= 32) clear_graphs();
+      if (graphs.size() >= 64) clear_graphs();
       GraphEntry g;
       const long long l0 = g_launches;
       cap_xnode = nullptr;
@@ -268,7 +271,7 @@ struct tsg_stream {
 
   // phase profiling (TSG_PROFILE): per-slice event sets, reused every
   // kProfSets slices (by then the slice's work has long completed)
-  static constexpr int kProfSets = 4;
+  static constexpr int kProfSets = 6;  // a multiple of kNP and of the 2-buffer ping-pong (bounded graph keys)
   cudaEvent_t pev[kProfSets][5] = {};
   bool pev_live[kProfSets] = {};
   int cur_q = -1;  // event set of the slice being enqueued (-1: none)
@@ -384,7 +387,7 @@ struct tsg_stream {
   // fused tail's per-CTA partials
   static constexpr long long kTailPart = 2LL * kMaxGrid * (kMaxD + 1);
   static constexpr long long kPartStride = kTailPart + (long long)kMaxD * kMaxGrid + 64;
-  DecideArgs last_da[2];  // partial layout of the last captured leading-mode pass
+  DecideArgs last_da[kNP];  // partial layout of the last captured leading-mode pass
   bool use_tail = std::getenv("TSG_NO_TAIL") == nullptr;
   // First mode handled by the fused tail kernel (d-1: none; the tail then
   // only decides): trailing modes with small inputs.
@@ -403,7 +406,7 @@ struct tsg_stream {
   // Partials for every mode plus one spare region, allocated once so that
   // pointers captured by enqueued kernels stay valid.
   void ensure_partial(long long n) {
-    const long long need = std::max(n, 2 * kPartStride);
+    const long long need = std::max(n, kNP * kPartStride);
     if (need <= partial_cap) return;
     if (partial) sync();
     dfree(partial);
@@ -607,8 +610,8 @@ struct tsg_stream {
     }
     if (!tile_ctr) tile_ctr = reinterpret_cast<unsigned*>(dalloc(kMaxD * 2));
     if (!tail_done) {
-      tail_done = reinterpret_cast<unsigned*>(dalloc(1));
-      ck(cudaMemsetAsync(tail_done, 0, 8, st), "memset");
+      tail_done = reinterpret_cast<unsigned*>(dalloc((kNP + 1) / 2));
+      ck(cudaMemsetAsync(tail_done, 0, 8 * ((kNP + 1) / 2), st), "memset");
       ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     }
   }
@@ -842,7 +845,7 @@ struct tsg_stream {
   };
   Pend prev;
   bool have_prev = false;
-  double* stage[2] = {nullptr, nullptr};  // host-slice staging per parity
+  double* stage[kNP] = {};  // host-slice staging per slot
 
   // Mode projections + decision of one slice on `st` (a cached graph: the
   // input pointer is read by the mode-0 kernel from mapped memory; the
@@ -860,7 +863,7 @@ struct tsg_stream {
     auto mbody = [&](bool cap) {
       const int saved = cur_q;
       cur_q = p.q;
-      wait_ev(st, ev_isvd[par], cap);  // buffers + slot last read by the insertion 2 slices ago
+      wait_ev(st, ev_isvd[par], cap);  // buffers + slot last read by the insertion kNP slices ago
       wait_ev(st, ev_h2d[par], cap);   // staged host slice
       long long yd[kMaxD];
       for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
@@ -975,7 +978,7 @@ struct tsg_stream {
     Pend cur;
     cur.t0 = std::chrono::steady_clock::now();
     cur.q = profiling() ? (int)(upd_count % kProfSets) : -1;
-    cur.par = (int)(upd_count++ & 1);
+    cur.par = (int)(upd_count++ % kNP);
     const double* y = y_in;
     const bool misaligned = (reinterpret_cast<uintptr_t>(y_in) & 15) != 0;
     if (mem_kind == TSG_MEM_HOST || misaligned) {
@@ -992,7 +995,8 @@ struct tsg_stream {
       ev_h2d_valid[cur.par] = true;
       y = stage[cur.par];
       // the caller's previous host slice has been consumed once its copy ends
-      if (ev_h2d_valid[cur.par ^ 1]) ck(cudaEventSynchronize(ev_h2d[cur.par ^ 1]), "h2d sync");
+      const int pp = (cur.par + kNP - 1) % kNP;
+      if (ev_h2d_valid[pp]) ck(cudaEventSynchronize(ev_h2d[pp]), "h2d sync");
     }
     // enqueue this slice first, then settle the previous one: the projection
     // stream never waits on the host
@@ -1500,7 +1504,7 @@ struct tsg_stream {
       upad[k] = nullptr;
       upad_R[k] = 0;
     }
-    stage[0] = stage[1] = nullptr;
+    for (auto& p : stage) p = nullptr;
     sh_send = sh_recv = sh_z = sh_stage = nullptr;
     sh_send_cap = sh_recv_cap = sh_stage_cap = 0;
     shard_world = 0;
@@ -1513,11 +1517,11 @@ struct tsg_stream {
     rec_read = 0;
     have_last_ctrl = false;
     for (auto& l : pev_live) l = false;
-    seq_expect[0] = seq_expect[1] = 0;
+    for (auto& q : seq_expect) q = 0;
     r_exact = 0;
     drift_pending = 0;
     upd_count = 0;
-    ev_isvd_valid[0] = ev_isvd_valid[1] = false;
+    for (auto& v : ev_isvd_valid) v = false;
     pipe_elems = 0;
     for (auto& set : pw)
       for (auto& b : set) b = nullptr;
@@ -1527,13 +1531,13 @@ struct tsg_stream {
     if (!si) ck(cudaStreamCreateWithFlags(&si, cudaStreamNonBlocking), "cudaStreamCreate");
     if (!sc) ck(cudaStreamCreateWithFlags(&sc, cudaStreamNonBlocking), "cudaStreamCreate");
     if (!s2) ck(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking), "cudaStreamCreate");
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < kNP; ++i)
       if (!ev_m0[i]) ck(cudaEventCreateWithFlags(&ev_m0[i], cudaEventDisableTiming), "event");
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kNP; ++i) {
       if (!ev_h2d[i]) ck(cudaEventCreateWithFlags(&ev_h2d[i], cudaEventDisableTiming), "event");
       ev_h2d_valid[i] = false;
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kNP; ++i) {
       if (!ev_proj[i]) ck(cudaEventCreateWithFlags(&ev_proj[i], cudaEventDisableTiming), "event");
       if (!ev_isvd[i]) ck(cudaEventCreateWithFlags(&ev_isvd[i], cudaEventDisableTiming), "event");
     }
@@ -1541,7 +1545,7 @@ struct tsg_stream {
       for (auto& e : set)
         if (!e) ck(cudaEventCreate(&e), "event");
     // every cross-stream event starts recorded, so graph wait nodes are valid
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kNP; ++i) {
       ck(cudaEventRecord(ev_h2d[i], st), "cudaEventRecord");
       ck(cudaEventRecord(ev_proj[i], st), "cudaEventRecord");
       ck(cudaEventRecord(ev_isvd[i], st), "cudaEventRecord");
@@ -1551,11 +1555,11 @@ struct tsg_stream {
     ck(cudaMallocHost(&ctrl_h, sizeof(Ctrl)), "cudaMallocHost");
     std::memset(ctrl_h, 0, sizeof(Ctrl));
     push_ctrl();
-    slots = reinterpret_cast<SliceCtl*>(dalloc(2 * ((sizeof(SliceCtl) + 7) / 8)));
-    ck(cudaMallocHost(&slots_h, 2 * sizeof(SliceCtl)), "cudaMallocHost");
-    std::memset(slots_h, 0, 2 * sizeof(SliceCtl));
-    ck(cudaHostAlloc(&hslot, 2 * sizeof(SliceCtl), cudaHostAllocMapped), "cudaHostAlloc");
-    std::memset(hslot, 0, 2 * sizeof(SliceCtl));
+    slots = reinterpret_cast<SliceCtl*>(dalloc(kNP * ((sizeof(SliceCtl) + 7) / 8)));
+    ck(cudaMallocHost(&slots_h, kNP * sizeof(SliceCtl)), "cudaMallocHost");
+    std::memset(slots_h, 0, kNP * sizeof(SliceCtl));
+    ck(cudaHostAlloc(&hslot, kNP * sizeof(SliceCtl), cudaHostAllocMapped), "cudaHostAlloc");
+    std::memset(hslot, 0, kNP * sizeof(SliceCtl));
     ck(cudaHostAlloc(&ring_h, sizeof(RecRing), cudaHostAllocMapped), "cudaHostAlloc");
     std::memset(ring_h, 0, sizeof(RecRing));
     void* dp = nullptr;
@@ -1563,8 +1567,8 @@ struct tsg_stream {
     hslot_d = static_cast<SliceCtl*>(dp);
     ck(cudaHostGetDevicePointer(&dp, ring_h, 0), "cudaHostGetDevicePointer");
     ring_d = static_cast<RecRing*>(dp);
-    seq_dev = reinterpret_cast<unsigned long long*>(dalloc(2));
-    ck(cudaMemsetAsync(seq_dev, 0, 2 * sizeof(unsigned long long), st), "memset");
+    seq_dev = reinterpret_cast<unsigned long long*>(dalloc(kNP));
+    ck(cudaMemsetAsync(seq_dev, 0, kNP * sizeof(unsigned long long), st), "memset");
     // grid-insertion handoff + handshake words (zeroed before any insertion)
     isvd_hand = dalloc(kHandDoubles);
     isvd_gsync = reinterpret_cast<unsigned*>(dalloc(2));
@@ -1573,16 +1577,16 @@ struct tsg_stream {
   }
 
   void destroy_streams() {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kNP; ++i) {
       if (ev_proj[i]) cudaEventDestroy(ev_proj[i]);
       if (ev_isvd[i]) cudaEventDestroy(ev_isvd[i]);
     }
     for (auto& set : pev)
       for (auto& e : set)
         if (e) cudaEventDestroy(e);
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < kNP; ++i)
       if (ev_h2d[i]) cudaEventDestroy(ev_h2d[i]);
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < kNP; ++i)
       if (ev_m0[i]) cudaEventDestroy(ev_m0[i]);
     if (si) cudaStreamDestroy(si);
     if (sc) cudaStreamDestroy(sc);
