@@ -1359,10 +1359,19 @@ struct tsg_stream {
     d = order;
     tau = t;
     const long long size = prod(dims, order);
-    double* X = dalloc(size);
-    ck(cudaMemcpyAsync(X, x, sizeof(double) * size,
-                       mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                       st), "init H2D");
+    // a device batch is read in place (never written): no second copy of what
+    // may be the largest buffer of the run (config 4: 72.5 GB)
+    const bool own_x = !(mem_kind == TSG_MEM_DEVICE && (reinterpret_cast<uintptr_t>(x) & 15) == 0);
+    double* X = const_cast<double*>(x);
+    if (own_x) {
+      X = dalloc(size);
+      ck(cudaMemcpyAsync(X, x, sizeof(double) * size,
+                         mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                         st), "init H2D");
+    }
+    auto drop_x = [&] {
+      if (own_x) dfree(X);
+    };
     double* nrm = dalloc(1 + 1024);
     launch_sumsq(X, size, nrm, nrm + 1, st);
     double xsq = 0.0;
@@ -1371,11 +1380,11 @@ struct tsg_stream {
     ck(cudaGetLastError(), "init norm");
     dfree(nrm);
     if (std::sqrt(xsq) == 0.0) {
-      dfree(X);
+      drop_x();
       fail(TSG_EINVAL, "stream_init: initial batch must be nonzero to seed a factorization");
     }
     if (!(t > 0.0 && t < 1.0)) {
-      dfree(X);
+      drop_x();
       fail(TSG_EINVAL, "sthosvd: tau must lie in (0, 1)");
     }
     // sthosvd (sthosvd.cpp:94-133)
@@ -1415,7 +1424,7 @@ struct tsg_stream {
       discarded += s.disc;
       sync();
       if (coreT != X) dfree(coreT);
-      else dfree(X);
+      else drop_x();
       coreT = nc;
       cd[k] = rk;
       if (k == order - 1) {

@@ -61,6 +61,12 @@ CONFIGS = {
     "c3": StreamConfig("c3", (512, 512, 512), (32, 32, 32), 32, 50, 5, 1e-3, 1e-4,
                        BASE_SEED + 3, spectrum_ratio=0.8,
                        notes="4-way, 50 slices of 512^3, core G x_k diag(0.8^i), R_t=32"),
+    # configs[3]: combustion-like 5-way stream of advected Gaussian blobs
+    # (the HCCI data itself is not in the container; see BlobStream)
+    "c4": StreamConfig("c4", (384, 384, 384, 16), (0, 0, 0, 0), 0, 100, 10, 1e-3, 1e-5,
+                       BASE_SEED + 4, extra={"kind": "blobs", "n_blobs": 64, "base_res": 384},
+                       notes="5-way combustion-like, 100 slices of 384^3 x 16 variables: tanh(a_k f + b_k) "
+                             "of 64 advected 3-D Gaussian blobs"),
     "c5": StreamConfig("c5", (256, 256, 256), (36, 36, 36), 36, 400, 10, 1e-4, 1e-6,
                        BASE_SEED + 5, growth=(8, 4, 50, 36),
                        notes="4-way rank growth 8->36 (+4 every 50 slices); nested core, R_t = active rank; init 10 (unspecified)"),
@@ -75,7 +81,14 @@ def scaled(cfg: StreamConfig, slice_dims: tuple, n_slices: int | None = None,
                         n_slices or cfg.n_slices, n_init or cfg.n_init, cfg.tau, cfg.eta,
                         cfg.seed, cfg.spectrum_ratio,
                         tuple(min(g, min(slice_dims)) for g in cfg.growth) if cfg.growth else (),
-                        cfg.notes + " (scaled)")
+                        cfg.notes + " (scaled)", dict(cfg.extra))
+
+
+def make_stream(cfg: StreamConfig):
+    """The generator a config names (Tucker-model streams, or advected blobs)."""
+    if cfg.extra.get("kind") == "blobs":
+        return BlobStream(cfg)
+    return TuckerStream(cfg)
 
 
 def _rng(seed: int, *stream: int) -> np.random.Generator:
@@ -192,3 +205,79 @@ class TuckerStream:
             x = x + (self.cfg.eta * torch.linalg.vector_norm(x) / torch.linalg.vector_norm(z)) * z
         # colexicographic flat: reverse dims then row-major flatten
         return x.permute(*reversed(range(x.ndim))).contiguous().reshape(-1)
+
+
+class BlobStream:
+    """Config 4 (BASELINE configs[3]): a combustion-like 5-way stream.
+
+    Base field f_t(x, y, z) = sum_b A_b exp(-|p - c_b - v_b t|^2 / (2 w_b^2))
+    over 64 seeded 3-D Gaussian blobs: centres uniform in the box, widths
+    U[8, 40] cells, velocities N(0, 1) cells/step, amplitudes N(0, 1), no wrap
+    (SURVEY §8(d) resolutions of the unspecified distributions). Variable k
+    of slice t is tanh(a_k f_t + b_k) with a_k, b_k ~ U(0.5, 2); noise
+    ||N_t|| = eta ||X_t|| as for every config. Lengths are in cells of the
+    384^3 base grid, so a reduced-resolution `scaled` config draws the same
+    field on a coarser grid. Each blob is separable, so f_t is a sum of 64
+    outer products (one (N x 64) x (64 x N^2) GEMM on the device).
+    """
+
+    def __init__(self, cfg: StreamConfig):
+        self.cfg = cfg
+        nb = int(cfg.extra.get("n_blobs", 64))
+        base = float(cfg.extra.get("base_res", 384))
+        dims = cfg.slice_dims[:3]
+        self.nvar = cfg.slice_dims[3]
+        g = _rng(cfg.seed, 5)
+        self.centres = g.uniform(0.0, base, (nb, 3))
+        self.widths = g.uniform(8.0, 40.0, nb)
+        self.vel = g.standard_normal((nb, 3))
+        self.amp = g.standard_normal(nb)
+        v = _rng(cfg.seed, 6)
+        self.a = v.uniform(0.5, 2.0, self.nvar)
+        self.b = v.uniform(0.5, 2.0, self.nvar)
+        # grid point i of a dimension with n points sits at (i + 0.5) base / n
+        self.coords = [(np.arange(n) + 0.5) * (base / n) for n in dims]
+
+    def profiles(self, t: int) -> list:
+        """Per dimension: (n_blobs x N) Gaussian factors of the blobs at time t."""
+        out = []
+        for d, xs in enumerate(self.coords):
+            c = self.centres[:, d] + self.vel[:, d] * t
+            out.append(np.exp(-((xs[None, :] - c[:, None]) ** 2) / (2.0 * self.widths[:, None] ** 2)))
+        return out
+
+    def clean_slice_numpy(self, t: int) -> np.ndarray:
+        gx, gy, gz = self.profiles(t)
+        f = np.einsum("b,bx,by,bz->xyz", self.amp, gx, gy, gz, optimize=True)
+        return np.stack([np.tanh(self.a[k] * f + self.b[k]) for k in range(self.nvar)], axis=3)
+
+    def noise_numpy(self, t: int) -> np.ndarray:
+        return _rng(self.cfg.seed, 4, t).standard_normal(self.cfg.slice_dims)
+
+    slice_numpy = TuckerStream.slice_numpy
+    init_numpy = TuckerStream.init_numpy
+    init_dims = TuckerStream.init_dims
+
+    def slice_torch(self, t: int, device, generator_seed: int | None = None):
+        """Slice t on `device` (fp64), flat colexicographic; same field as
+        slice_numpy up to rounding, torch Philox noise (not bit-equal)."""
+        import torch
+        gx, gy, gz = [torch.as_tensor(p, dtype=torch.float64, device=device) for p in self.profiles(t)]
+        nx, ny, nz = gx.shape[1], gy.shape[1], gz.shape[1]
+        amp = torch.as_tensor(self.amp, dtype=torch.float64, device=device)
+        # colexicographic (x fastest): F[z, y, x] = sum_b (A gz)[b, z] gy[b, y] gx[b, x]
+        zy = ((amp[:, None] * gz)[:, :, None] * gy[:, None, :]).reshape(gx.shape[0], nz * ny)
+        f = (zy.t() @ gx).reshape(nz, ny, nx)  # (z, y, x) row-major == colexicographic (x, y, z)
+        x = torch.empty((self.nvar, nz, ny, nx), dtype=torch.float64, device=device)
+        for k in range(self.nvar):
+            torch.tanh(f * float(self.a[k]) + float(self.b[k]), out=x[k])
+        del f, zy
+        if self.cfg.eta > 0:
+            gen = torch.Generator(device=device)
+            gen.manual_seed((self.cfg.seed * 1_000_003 + t) & 0x7FFFFFFFFFFFFFFF
+                            if generator_seed is None else generator_seed)
+            xn = torch.linalg.vector_norm(x)
+            z = torch.randn(x.shape, dtype=torch.float64, device=device, generator=gen)
+            x.add_(z, alpha=float(self.cfg.eta * xn / torch.linalg.vector_norm(z)))
+            del z
+        return x.reshape(-1)

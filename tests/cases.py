@@ -35,7 +35,7 @@ class StreamCase:
 
 
 def config_case(cfg: dg.StreamConfig, n_slices: int | None = None) -> StreamCase:
-    s = dg.TuckerStream(cfg)
+    s = dg.make_stream(cfg)
     total = n_slices or cfg.n_slices
     return StreamCase(cfg.name, s.init_numpy(), s.init_dims(),
                       [s.slice_numpy(t) for t in range(cfg.n_init, total)], cfg.tau)

@@ -210,3 +210,31 @@ def test_config3_generator_midsize_vs_oracle(oracle):
     sc = P.compare_states(sg, so)
     print("c3_96", mc, sc)
     P.assert_parity(mc, sc)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_config4_generator_reduced_vs_oracle(oracle, asynchronous):
+    """Config-4 generator (5-way, advected blobs through tanh, 16 variables)
+    at 48^3 x 16: basis growth on most slices, ISVD width n ~ 3e5 (the large
+    insertion path), SURVEY §8(c)'s reduced-resolution parity for C4."""
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.scaled(dg.CONFIGS["c4"], (48, 48, 48, 16), n_slices=16, n_init=10, name="c4_48")
+    case = cases.config_case(cfg)
+    st = run_gpu(case, asynchronous=asynchronous)
+    ho = _oracle_run(oracle, case)
+    sg, so = st.export(), ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(st.metrics(), sg.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(sg, so)
+    print("c4_48", mc, sc)
+    assert int(np.count_nonzero(P.metrics_arrays(ho.metrics(), so.order)["expanded_mask"])) >= 2
+    # Every state field is held to 1e-10. The mode residuals are held to
+    # 5e-8: this generator grows all three spatial bases on most slices with
+    # Gram spectra clustered at the cut, so the weakest added columns are only
+    # determined to ~1e-8 by ANY eigensolver (raw factor columns differ from
+    # the reference's by ~2e-8 here, its sigma-weighted factors by ~4e-11),
+    # and each later slice's residual ||(I - U U^T) y|| (~4e-4 ||y||, just
+    # below delta) is measured against those columns.
+    assert sc["factors_raw"] <= 1e-7, sc
+    P.assert_parity(mc, sc, resid_tol=5e-8)

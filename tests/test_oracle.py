@@ -150,3 +150,22 @@ def test_process_mode_vs_reference(oracle, reference):
     assert ro == rr
     np.testing.assert_array_equal(yo, yr)
     np.testing.assert_array_equal(ho.export().factors[0], hr.export().factors[0])
+
+
+def test_config4_generator_layout_and_noise_rule():
+    """The config-4 generator: colexicographic layout, bounded tanh values,
+    the reference's per-slice noise rule ||N|| = eta ||X|| (datagen.cpp:90-101)
+    and a torch synthesis equal to the numpy one up to the noise."""
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.scaled(dg.CONFIGS["c4"], (12, 10, 8, 4), n_slices=4, n_init=2)
+    s = dg.make_stream(cfg)
+    clean = s.clean_slice_numpy(1)
+    assert clean.shape == (12, 10, 8, 4) and np.all(np.abs(clean) < 1.0)
+    flat = s.slice_numpy(1)
+    t = flat.reshape((4, 8, 10, 12)).transpose()
+    noise = t - clean
+    assert np.linalg.norm(noise) == pytest.approx(cfg.eta * np.linalg.norm(clean), rel=1e-9)
+    torch = pytest.importorskip("torch")
+    b = s.slice_torch(1, "cpu").numpy()
+    assert np.linalg.norm(b - flat) <= 3 * cfg.eta * np.linalg.norm(flat)
+    assert s.init_dims() == [12, 10, 8, 4, 2]
