@@ -13,7 +13,7 @@ __device__ __forceinline__ void decide_finish(const DecideArgs& a, double xsq, c
   SliceCtl* c = a.slot;
   double delta, slice_sq = 0.0;
   int zero = 0;
-  if (a.first_mode == 0) {
+  if (a.first_mode == 0 && !a.keep_delta) {
     slice_sq = xsq;
     zero = (xsq == 0.0);
     const double slice_norm = sqrt(xsq);

@@ -1731,7 +1731,7 @@ struct tsg_stream {
     da.off[mode] = 0;
     da.cnt[mode] = project(yb, yd, mode, pb, partial);
     da.first_mode = mode;
-    // decide() computes delta only for first_mode == 0; set it explicitly
+    da.keep_delta = 1;  // the caller's delta (streaming.hpp:69-70), also for mode 0
     slots_h[0].delta = delta;
     ck(cudaMemcpyAsync(&slots[0].delta, &slots_h[0].delta, 8, cudaMemcpyHostToDevice, st), "delta");
     launch_decide(da, st);

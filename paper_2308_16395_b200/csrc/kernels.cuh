@@ -102,6 +102,7 @@ struct DecideArgs {
   int first_mode;            // first mode evaluated by this decide call
   double tau;
   int order;
+  int keep_delta = 0;        // use slot->delta as given (process_nonstreaming_mode)
 };
 void launch_decide(const DecideArgs& a, cudaStream_t st);
 

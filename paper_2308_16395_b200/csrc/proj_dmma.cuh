@@ -1020,7 +1020,11 @@ inline int launch_rt(const ProjArgs& a, int streaming_in, cudaStream_t st) {
       if (g > 0) return g;
     }
   }
-  return launch_t<RT, pick_mc(RT, GM), GM, 0>(a, streaming_in, st);
+  const int g = launch_t<RT, pick_mc(RT, GM), GM, 0>(a, streaming_in, st);
+  if constexpr (pick_mc(RT, GM) > 1) {
+    if (g < 0) return launch_t<RT, 1, GM, 0>(a, streaming_in, st);  // smaller reduction area
+  }
+  return g;
 }
 
 // Picks (RT, MC, GM); returns -1 when the shape is outside the DMMA kernel's
@@ -1074,8 +1078,9 @@ inline int launch(const ProjArgs& a, int streaming_in, cudaStream_t st) {
   if (a.v.left * a.v.right >= (1LL << 31) || a.v.left >= (1LL << 31)) return -1;
   const int RT = (a.R + 7) / 8;
   const long long ngroups = (N + 7) / 8;
-  const long long smem = 8 * (ngroups * 8 * (8 * RT + 4)) + 8LL * 9 * 4 * RT * 2 * 32;
-  if (smem > 220 * 1024) return -1;
+  // the U image alone must fit; launch_t checks the exact footprint of the
+  // (MC, stages) variant it picks (the reduction area depends on MC)
+  if (8 * (ngroups * 8 * (8 * RT + 4)) > 200 * 1024) return -1;
   const int GM = (int)((ngroups + 7) / 8);
   if (GM <= 1) return dispatch_rt<1>(a, streaming_in, st);
   if (GM <= 2) return dispatch_rt<2>(a, streaming_in, st);

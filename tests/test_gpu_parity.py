@@ -238,3 +238,41 @@ def test_config4_generator_reduced_vs_oracle(oracle, asynchronous):
     # below delta) is measured against those columns.
     assert sc["factors_raw"] <= 1e-7, sc
     P.assert_parity(mc, sc, resid_tol=5e-8)
+
+
+@pytest.mark.parametrize("slice_dims,ranks", [
+    ((384, 48, 24, 16), (41, 20, 10, 4)),    # C4-like: N = 384, R0 in (40, 48]
+    ((384, 40, 16), (63, 12, 5)),            # R0 beyond the DMMA envelope (generic kernel)
+    ((512, 36, 20), (32, 30, 7)),            # C3-like N = 512
+    ((200, 200, 12), (10, 10, 3)),           # C2-like, TMA mode-0 path
+    ((256, 30, 9), (36, 17, 9)),             # C5 late
+])
+def test_process_mode_shapes_vs_numpy(slice_dims, ranks):
+    """Every projection kernel variant the engine dispatches to (TMA mode 0,
+    register / ring DMMA with RT up to 8, the generic kernel): the projected
+    tensor and the residual norm ||Y - U U^T Y|| of process_nonstreaming_mode
+    against float64 numpy, mode by mode, on a state built with
+    assemble_streaming_state."""
+    g = np.random.default_rng(11)
+    d = len(slice_dims) + 1
+    facs = [np.linalg.qr(g.standard_normal((n, r)))[0] for n, r in zip(slice_dims, ranks)]
+    n = int(np.prod(ranks))
+    r = 2
+    q = np.linalg.qr(g.standard_normal((n, r)))[0]
+    sig = np.array([2.0, 1.0])
+    left = np.linalg.qr(g.standard_normal((3, r)))[0]
+    st_in = S.State(order=d, n_d=3, rank=r, insertions=0, core_dims=tuple(ranks) + (r,),
+                    slice_dims=tuple(slice_dims), tau=0.1, squared_error=0.0, total_input_sq=1.0,
+                    nonstream_discarded_sq=0.0, core=(q * sig[None, :]).ravel(order="F"),
+                    factors=facs, sigma=sig, left=left, right=q)
+    st = S.assemble_streaming_state(st_in)
+    y = g.standard_normal(slice_dims)
+    for k in range(d - 1):
+        res, yo = st.process_nonstreaming_mode(y, k, 1e300)
+        u = facs[k]
+        p = np.moveaxis(np.tensordot(u.T, y, axes=([1], [k])), 0, k)
+        e = y - np.moveaxis(np.tensordot(u, p, axes=([1], [k])), 0, k)
+        assert yo.shape == p.shape
+        np.testing.assert_allclose(yo, p, rtol=0, atol=1e-12 * np.abs(p).max())
+        assert res == pytest.approx(np.linalg.norm(e), rel=1e-12), (k, res, np.linalg.norm(e))
+        y = p
