@@ -254,6 +254,16 @@ def run_ours(args, world, rank, local):
     step_s = ms_max / 1e3 / args.steps
     step_roof = max(sb / (hbm * 1e9), sf / (dmma * 1e12))
 
+    # verification on sampled slices: the device
+    # reconstruction of the last timed slices against the slices themselves
+    samp = min(4, nsl)
+    num = den = 0.0
+    for i in range(nsl - samp, nsl):
+        a_, b_ = st.error_sums(slices[i], cfg.n_init + i, 1)
+        num, den = num + a_, den + b_
+    sampled = {"slices": samp, "relative_error": float(np.sqrt(num / den)) if den > 0 else 0.0,
+               "ledger_estimate": st.estimate_relative_error(), "tau": cfg.tau}
+
     # end to end through the public API with pinned host slices, continuing
     # the same state (H2D on the engine's copy stream inside the timed region)
     e2e = None
@@ -304,6 +314,7 @@ def run_ours(args, world, rank, local):
         "phases_ms": {k: v for k, v in prof.items() if k != "updates"},
         "fp64_peak_tflops": {"dmma": dmma, "dfma": dfma},
         "clocks": clk, "gpu_launches": launches, "e2e": e2e, "cpu_baseline": cpu,
+        "sampled_verification": sampled,
     }
     st.close()
     return out

@@ -13,6 +13,9 @@
  *   tsg_import_state    <- tucker::assemble_streaming_state  streaming.hpp:85-87
  *   tsg_export_state    <- StreamingState fields + streaming_factor()
  *                                                            streaming.hpp:34-49
+ *   tsg_reconstruct / tsg_error_sums
+ *                       <- reconstruct / relative_error     sthosvd.hpp:51,55
+ *                          of StreamingState::full_model()  streaming.hpp:48-49
  *   tsg_shard_setup / tsg_shard_begin / tsg_shard_continue
  *                       <- stream_update split over G GPUs (no reference
  *                          counterpart; see the sharded section below)
@@ -128,6 +131,19 @@ double tsg_estimate_relative_error(tsg_stream* h);
 int64_t tsg_metrics_count(tsg_stream* h);
 int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out);
 int tsg_last_metrics(tsg_stream* h, tsg_slice_metrics* out);
+
+/* ---- Reconstruction (reconstruct / relative_error, sthosvd.hpp:51,55, of
+ * StreamingState::full_model(), streaming.hpp:48-49), slice range by slice
+ * range so full-size streams can be verified on sampled slices.
+ * tsg_reconstruct writes slices [t0, t0+count) of the model, colexicographic
+ * N_0 x ... x N_{d-2} x count, to `out` (host or device per mem_kind).
+ * tsg_error_sums returns ||x - X||^2 and ||x||^2 over those slices for the
+ * caller's slices x (same layout); relative_error over the whole stream is
+ * sqrt(sum num / sum den) (zero-norm rules as in sthosvd.cpp:151-156). */
+int tsg_reconstruct(tsg_stream* h, int64_t t0, int64_t count, double* out,
+                    int32_t mem_kind);
+int tsg_error_sums(tsg_stream* h, const double* x, int64_t t0, int64_t count,
+                   int32_t mem_kind, double* num_sq, double* den_sq);
 
 /* ---- Sharded update (one process per GPU).
  *

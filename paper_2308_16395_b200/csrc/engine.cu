@@ -1707,6 +1707,75 @@ struct tsg_stream {
     initialized = true;
   }
 
+  // ------------------------------------------------------ reconstruction
+  // Slices [t0, t0 + count) of full_model() (streaming.hpp:48-49) into the
+  // device buffer `out` (colexicographic N_0 x .. x N_{d-2} x count).
+  void reconstruct_dev(long long t0, long long count, double* out) {
+    flush();
+    const long long nd = ctrl_h->n_d;
+    if (t0 < 0 || count < 0 || t0 + count > nd)
+      fail(TSG_EINVAL, "reconstruct: slice range outside [0, n_d)");
+    if (count == 0) return;
+    const int r = ctrl_h->r;
+    const long long n = n_rows();
+    long long dims[kMaxD];
+    for (int k = 0; k + 1 < d; ++k) dims[k] = R[k];
+    const long long total = slice_elems * count;
+    double* a = dalloc(total);
+    double* b = dalloc(total);
+    launch_recon_core(core, n, r, left, capr, t0, count, a, st);
+    double* cur = a;
+    for (int k = 0; k + 1 < d; ++k) {
+      const long long lft = prod(dims, k);
+      const long long rgt = prod(dims + k + 1, d - 2 - k) * count;
+      double* dst = (k + 2 == d) ? out : (cur == a ? b : a);
+      launch_recon_expand(cur, lft, (int)R[k], rgt, U[k], N[k], dst, st);
+      dims[k] = N[k];
+      cur = dst;
+    }
+    ck(cudaStreamSynchronize(st), "reconstruct");
+    ck(cudaGetLastError(), "reconstruct");
+    dfree(a);
+    dfree(b);
+  }
+  void reconstruct(long long t0, long long count, double* out, int mem_kind) {
+    if (mem_kind == TSG_MEM_DEVICE) {
+      reconstruct_dev(t0, count, out);
+      return;
+    }
+    double* tmp = dalloc(std::max(1LL, slice_elems * count));
+    reconstruct_dev(t0, count, tmp);
+    ck(cudaMemcpy(out, tmp, sizeof(double) * slice_elems * count, cudaMemcpyDeviceToHost), "D2H");
+    dfree(tmp);
+  }
+  // ||x - X||^2 and ||x||^2 over slices [t0, t0 + count) of full_model()
+  // (relative_error, sthosvd.cpp:148-160, accumulated per slice range).
+  void error_sums(const double* x, long long t0, long long count, int mem_kind, double* num_sq,
+                  double* den_sq) {
+    const long long total = slice_elems * count;
+    double* rec = dalloc(std::max(1LL, total));
+    reconstruct_dev(t0, count, rec);
+    const double* xd = x;
+    double* xc = nullptr;
+    if (mem_kind == TSG_MEM_HOST) {
+      xc = dalloc(std::max(1LL, total));
+      ck(cudaMemcpy(xc, x, sizeof(double) * total, cudaMemcpyHostToDevice), "H2D");
+      xd = xc;
+    }
+    double* part = dalloc(4 * kNumSMs + 2);
+    double hs[2] = {0.0, 0.0};
+    if (total > 0) {
+      launch_diff_sumsq(xd, rec, total, part, part + 4 * kNumSMs, st);
+      ck(cudaMemcpyAsync(hs, part + 4 * kNumSMs, 16, cudaMemcpyDeviceToHost, st), "D2H");
+      ck(cudaStreamSynchronize(st), "error sums");
+    }
+    *num_sq = hs[0];
+    *den_sq = hs[1];
+    dfree(part);
+    if (xc) dfree(xc);
+    dfree(rec);
+  }
+
   // process_nonstreaming_mode (streaming.cpp:126-155) on a host tensor.
   double process_mode(const double* y_h, const long long* ydims, int mode, double delta,
                       double* y_out, long long cap, long long* ydims_out) {
@@ -1873,6 +1942,24 @@ int tsg_init(tsg_stream* h, const double* x, int32_t order, const int64_t* dims,
 
 int tsg_update(tsg_stream* h, const double* slice, int32_t mem_kind) {
   return guarded(h, [&] { h->update(slice, mem_kind); });
+}
+
+int tsg_reconstruct(tsg_stream* h, int64_t t0, int64_t count, double* out, int32_t mem_kind) {
+  return guarded(h, [&] {
+    if (!out && count > 0) fail(TSG_EINVAL, "reconstruct: null output");
+    h->reconstruct(t0, count, out, mem_kind);
+  });
+}
+
+int tsg_error_sums(tsg_stream* h, const double* x, int64_t t0, int64_t count, int32_t mem_kind,
+                   double* num_sq, double* den_sq) {
+  return guarded(h, [&] {
+    if ((!x && count > 0) || !num_sq || !den_sq) fail(TSG_EINVAL, "relative_error: null argument");
+    h->flush();
+    if (t0 < 0 || count < 0 || t0 + count > h->ctrl_h->n_d)
+      fail(TSG_EINVAL, "relative_error: slice range outside [0, n_d)");
+    h->error_sums(x, t0, count, mem_kind, num_sq, den_sq);
+  });
 }
 
 int tsg_shard_setup(tsg_stream* h, int32_t rank, int32_t world, const int64_t* bounds) {

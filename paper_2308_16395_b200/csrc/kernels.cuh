@@ -183,6 +183,17 @@ void launch_coupling_check(Ctrl* ctrl, const double* core, const double* q,
 
 int measure_fp64_peaks(int device, double* dmma_tflops, double* dfma_tflops);
 
+// ------------------------------------------------- reconstruction (recon.cu)
+// z (n x count) = core_mat (n x r) * left[t0 .. t0+count)^T (left row-major, ld capr)
+void launch_recon_core(const double* core, long long n, int r, const double* left, int capr,
+                       long long t0, long long count, double* z, cudaStream_t st);
+// out (left, N, right) = U (N x R) along the middle mode of z (left, R, right)
+void launch_recon_expand(const double* z, long long left, int R, long long right, const double* u,
+                         long long N, double* out, cudaStream_t st);
+// out[0] = ||x - y||^2, out[1] = ||x||^2 (part: 4 * kNumSMs doubles)
+void launch_diff_sumsq(const double* x, const double* y, long long n, double* part, double* out,
+                       cudaStream_t st);
+
 // ------------------------------------------------------ sharded update
 constexpr int kMaxShards = 64;
 // Partial pairs of the locally projected modes (layout as in DecideArgs).

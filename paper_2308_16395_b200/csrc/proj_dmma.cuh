@@ -269,9 +269,14 @@ __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb
       }
     }
     // ---- cross-warp reduction (reduce-scatter then gather; fixed order)
+    // the next tile index is read right after the barrier that publishes it:
+    // thread 0 rewrites s_next in the next iteration before that iteration's
+    // first barrier, so reading it at the end of this one would race
+    long long next_pub = 0;
     if (a.debug_skip & 2) {  // profiling only
       if (dyn && threadIdx.x == 0) s_next = after;
       __syncthreads();
+      next_pub = s_next;
     } else {
     double* myred = red + warp * (PER * 32);
 #pragma unroll
@@ -282,6 +287,7 @@ __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb
         for (int i = 0; i < 2; ++i) myred[((mc * RT + rt) * 2 + i) * 32 + lane] = acc[mc][rt][i];
     if (dyn && threadIdx.x == 0) s_next = after;
     __syncthreads();
+    next_pub = s_next;
     double* fin = red + NW * (PER * 32);
     for (int slot = warp; slot < PER; slot += NW) {
       double sacc = 0.0;
@@ -382,7 +388,7 @@ __global__ void __launch_bounds__(32 * NW, STAGES > 0 ? 1 : (NW == 8 ? pick_minb
       tile += gridDim.x;  // static schedule: the ring prefetches by stride
     } else {
       tile = next;
-      next = dyn ? s_next : tile + gridDim.x;
+      next = dyn ? next_pub : tile + gridDim.x;
     }
   }
   racc = block_sum(racc, sred);

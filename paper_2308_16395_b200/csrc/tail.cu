@@ -11,6 +11,8 @@
 // partial sums are reduced in a fixed order by CTA 0, which then decides.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "decide.cuh"
 #include "kernels.cuh"
 
@@ -219,7 +221,13 @@ int launch_t(const TailArgs& t, cudaStream_t st) {
       per_sm < 1)
     return -1;
   long long grid = (fmax + 7) / 8;
-  const long long cap = kNumSMs;  // one CTA per SM: short launch ramp, cheap grid barrier
+  // one CTA per SM: short launch ramp, cheap grid barrier (TSG_TAIL_CTAS:
+  // a smaller grid that fits next to a capped mode-0 grid)
+  static const long long cap_env = [] {
+    const char* e = std::getenv("TSG_TAIL_CTAS");
+    return e ? std::atoll(e) : 0LL;
+  }();
+  const long long cap = cap_env > 0 ? cap_env : kNumSMs;
   if (grid > cap) grid = cap;
   if (grid > kMaxGrid) grid = kMaxGrid;
   if (grid < 1) grid = 1;

@@ -100,7 +100,8 @@ EXPORTED = [
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
     "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
-    "tsg_shard_setup", "tsg_shard_begin", "tsg_shard_continue",
+    "tsg_shard_setup", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
+    "tsg_error_sums",
 ]
 
 _LIB = None
@@ -153,6 +154,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.tsg_shard_setup.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _i64p]
     L.tsg_shard_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TsgExchange)]
     L.tsg_shard_continue.argtypes = [C.c_void_p, C.POINTER(TsgExchange)]
+    L.tsg_reconstruct.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]
+    L.tsg_error_sums.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, _dp, _dp]
     _LIB = L
     return L
 
@@ -326,6 +329,31 @@ class StreamingState:
     def estimate_relative_error(self) -> float:
         return float(self.L.tsg_estimate_relative_error(self.h))
 
+    def reconstruct(self, t0: int = 0, count: int | None = None, out=None):
+        """Slices [t0, t0+count) of full_model() (reconstruct, sthosvd.cpp:135-146),
+        flat colexicographic. `out` may be a CUDA torch tensor (filled on the
+        device); otherwise a numpy array is returned."""
+        q = self.query()
+        if count is None:
+            count = q["n_d"] - t0
+        n = int(np.prod(q["slice_dims"])) * count
+        if out is None:
+            out = np.zeros(max(n, 1))
+            ptr, kind = _pointer(out)
+            self._check(self.L.tsg_reconstruct(self.h, t0, count, ptr, kind))
+            return out[:n]
+        ptr, kind = _pointer(out)
+        self._check(self.L.tsg_reconstruct(self.h, t0, count, ptr, kind))
+        return out
+
+    def error_sums(self, x, t0: int, count: int) -> tuple[float, float]:
+        """(||x - X||^2, ||x||^2) over slices [t0, t0+count) for the caller's
+        flat slices x (numpy or CUDA torch)."""
+        ptr, kind = _pointer(x)
+        a, b = C.c_double(), C.c_double()
+        self._check(self.L.tsg_error_sums(self.h, ptr, t0, count, kind, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def profile(self, reset: bool = False) -> dict:
         out = np.zeros(6)
         self._check(self.L.tsg_profile(self.h, _p(out), 6, int(reset)))
@@ -381,6 +409,21 @@ def stream_update(state: StreamingState, y) -> None:
 
 def process_nonstreaming_mode(state: StreamingState, y, mode: int, delta: float):
     return state.process_nonstreaming_mode(y, mode, delta)
+
+
+def relative_error(x, state: StreamingState) -> float:
+    """relative_error(x, state.full_model()) (sthosvd.cpp:148-160) for the
+    whole stream x (flat colexicographic, n_d slices; numpy or CUDA torch)."""
+    q = state.query()
+    per = int(np.prod(q["slice_dims"]))
+    if len(x) != per * q["n_d"]:
+        raise InvalidArgument(1, "relative_error: shape mismatch")
+    num, den = state.error_sums(x, 0, q["n_d"])
+    if den == 0.0:
+        if num == 0.0:
+            return 0.0
+        raise InvalidArgument(1, "relative_error: zero-norm input with nonzero reconstruction")
+    return float(np.sqrt(num) / np.sqrt(den))
 
 
 def estimate_relative_error(state: StreamingState) -> float:

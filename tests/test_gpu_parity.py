@@ -276,3 +276,103 @@ def test_process_mode_shapes_vs_numpy(slice_dims, ranks):
         np.testing.assert_allclose(yo, p, rtol=0, atol=1e-12 * np.abs(p).max())
         assert res == pytest.approx(np.linalg.norm(e), rel=1e-12), (k, res, np.linalg.norm(e))
         y = p
+
+
+def test_reconstruct_and_relative_error_vs_numpy():
+    """Device reconstruct of full_model() slices and relative_error
+    (sthosvd.cpp:135-160) against numpy on the exported state; the ledger
+    estimate bounds the true error."""
+    case = cases.case_growth()
+    st = run_gpu(case)
+    e = st.export()
+    full = P.reconstruct(e)                       # numpy (N_0, ..., N_{d-2}, n_d)
+    flat = np.ascontiguousarray(full.transpose()).ravel()
+    got = st.reconstruct()
+    np.testing.assert_allclose(got, flat, rtol=0, atol=1e-12 * np.abs(flat).max())
+    per = int(np.prod(e.slice_dims))
+    part = st.reconstruct(3, 2)
+    np.testing.assert_array_equal(part, got[3 * per:5 * per])
+    x = np.concatenate([case.init_flat] + list(case.slices))
+    ref = np.linalg.norm(x - flat) / np.linalg.norm(x)
+    rel = S.relative_error(x, st)
+    assert rel == pytest.approx(ref, rel=1e-10)
+    assert rel <= st.estimate_relative_error() * (1 + 1e-9)
+    with pytest.raises(S.InvalidArgument):
+        st.reconstruct(e.n_d - 1, 2)
+
+
+@pytest.mark.parametrize("slice_dims,ranks", [
+    ((320, 20, 8), (35, 10, 4)),
+    ((320, 160, 16), (35, 20, 4)),
+    ((384, 64, 40), (41, 20, 6)),
+    ((384, 12, 6, 4), (41, 6, 3, 2)),
+    ((200, 30, 6), (10, 8, 3)),
+    ((512, 10, 4), (32, 5, 2)),
+])
+def test_process_mode_growth_shapes_vs_oracle(oracle, slice_dims, ranks):
+    """Basis growth through process_nonstreaming_mode (streaming.cpp:126-155)
+    on every mode, large mode-0 sizes included, against the checker on the
+    same assembled state: residual, grown basis (sigma-weighted), output."""
+    import py_oracle
+    g = np.random.default_rng(17)
+    d = len(slice_dims) + 1
+    facs = [np.linalg.qr(g.standard_normal((n, r)))[0] for n, r in zip(slice_dims, ranks)]
+    n = int(np.prod(ranks))
+    r = 2
+    q = np.linalg.qr(g.standard_normal((n, r)))[0]
+    sig = np.array([2.0, 1.0])
+    left = np.linalg.qr(g.standard_normal((3, r)))[0]
+    kw = dict(order=d, n_d=3, rank=r, insertions=0, core_dims=tuple(ranks) + (r,),
+              slice_dims=tuple(slice_dims), tau=0.1, squared_error=0.0, total_input_sq=1.0,
+              nonstream_discarded_sq=0.0, core=(q * sig[None, :]).ravel(order="F"),
+              factors=facs, sigma=sig, left=left, right=q)
+    st = S.assemble_streaming_state(S.State(**kw))
+    ho = oracle.assemble(py_oracle.State(**kw))
+    # a slice with structure outside the current bases plus noise
+    extra = [np.linalg.qr(g.standard_normal((nn, 3)))[0] for nn in slice_dims]
+    y = np.einsum("abc,ia,jb,kc->ijk", g.standard_normal((3, 3, 3)), *extra[:3]) if d == 4 else None
+    if d == 5:
+        y = np.einsum("abcd,ia,jb,kc,ld->ijkl", g.standard_normal((3, 3, 3, 3)), *extra)
+    y = y / np.linalg.norm(y) + 1e-3 * g.standard_normal(slice_dims) / np.sqrt(y.size)
+    delta = 1e-4 * np.linalg.norm(y)
+    for k in range(d - 1):
+        res, yo = st.process_nonstreaming_mode(y, k, delta)
+        ro, yr = ho.process_nonstreaming_mode(y, k, delta)
+        assert res == pytest.approx(ro, rel=1e-10), (k, res, ro)
+        assert yo.shape == yr.shape, (k, yo.shape, yr.shape)
+        # the carried coefficients of the weakest new directions are set by
+        # near-cut eigenvectors (defined to ~1e-8): sigma-level tolerance
+        np.testing.assert_allclose(yo, yr, rtol=0, atol=1e-7 * np.abs(yr).max())
+        y = yr
+    a, b = st.export(), ho.export()
+    for fa, fb in zip(a.factors, b.factors):
+        assert fa.shape == fb.shape
+        da = np.max(np.abs(fa.T @ fa - np.eye(fa.shape[1])))
+        db = np.max(np.abs(fb.T @ fb - np.eye(fb.shape[1])))
+        # weak added directions are as (non-)orthogonal for the checker (db)
+        assert da <= max(10 * db, 1e-9), (da, db)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("graphs", [True, False])
+def test_config4_wide_mode0_vs_oracle(oracle, graphs, monkeypatch):
+    """Config-4 generator with a 320-wide mode 0 (the register DMMA projection
+    with dynamic tile scheduling, RT = 5, GM = 8) through basis growth: the
+    regression case of the tile-index race fixed in proj_dmma_kernel (a thread
+    could read the next tile index after thread 0 had already published the
+    one after it, so a CTA's threads split across tiles and wrote stale
+    residual columns)."""
+    from paper_2308_16395_b200 import datagen as dg
+    if not graphs:
+        monkeypatch.setenv("TSG_NO_GRAPH", "1")
+    cfg = dg.scaled(dg.CONFIGS["c4"], (320, 40, 40, 16), n_slices=12, n_init=10, name="c4_wide")
+    case = cases.config_case(cfg)
+    st = run_gpu(case)
+    ho = _oracle_run(oracle, case)
+    sg, so = st.export(), ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(st.metrics(), sg.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(sg, so)
+    print("c4_wide", graphs, mc, sc)
+    assert sc["factors_raw"] <= 1e-7, sc
+    P.assert_parity(mc, sc, resid_tol=5e-8)

@@ -9,7 +9,8 @@ L = S.load_library()
 L.tsg_debug_project.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_void_p, C.c_int32,
                                 C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_double)]
 dev = torch.device("cuda", 0)
-shapes = [(1, 384, 20000, 41), (1, 384, 20000, 36), (40, 384, 300, 41), (1, 384, 5000, 63),
+shapes = [(1, 320, 200000, 22), (1, 320, 20000, 22), (7, 96, 96, 20), (1, 96, 2000, 20), (1, 320, 20000, 35),
+          (1, 320, 20000, 12), (1, 384, 20000, 41), (1, 384, 20000, 36), (40, 384, 300, 41), (1, 384, 5000, 63),
           (63, 384, 100, 98), (1, 512, 3000, 32), (1, 200, 4000, 10), (7, 96, 96, 20), (1, 256, 3000, 36),
           (1, 48, 2000, 38)]
 bad = 0
@@ -26,5 +27,6 @@ for (left, n, right, R) in shapes:
     err = (got - ref).norm() / ref.norm()
     ok = rc == 0 and err < 1e-12
     bad += not ok
-    print(f"left={left} N={n} right={right} R={R}: rc={rc} relerr={err:.2e} {'ok' if ok else 'BAD'} {ms.value*1e3:.1f}us")
+    msg = "" if rc == 0 else L.tsg_last_error(None).decode()
+    print(f"left={left} N={n} right={right} R={R}: rc={rc} relerr={err:.2e} {'ok' if ok else 'BAD'} {ms.value*1e3:.1f}us {msg}")
 print("bad", bad)
