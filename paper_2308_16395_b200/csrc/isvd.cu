@@ -170,7 +170,7 @@ __device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sU) {
   S.idx = si;
   S.perm = si + 32;
   S.flag = si + 64;
-  const int iters = secular::eig_rank_one(m, sd, sz, S, lam, W, sG);
+  const int iters = secular::eig_rank_one_fast<RM>(m, sd, sz, S, lam, W, sG);
   TSG_CLK(5);
   int rank = 0;
   if (lane == 0) rank = inner_truncate(io, lam, m, iters);
