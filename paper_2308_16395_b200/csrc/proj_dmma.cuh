@@ -421,8 +421,12 @@ inline int launch_t(const ProjArgs& a, int streaming_in, cudaStream_t st) {
   }
   const long long cols = a.v.left * a.v.right;
   const long long ntiles = (cols + 8 * MC - 1) / (8 * MC);
-  // one SM is left to the concurrently running insertion kernel
-  const long long slots = (long long)(kNumSMs - 1) *
+  // SMs left to the concurrently running insertion kernels (TSG_PROJ_FREE_SMS)
+  static const int free_sms = [] {
+    const char* e = std::getenv("TSG_PROJ_FREE_SMS");
+    return e ? std::atoi(e) : 1;
+  }();
+  const long long slots = (long long)(kNumSMs - free_sms) *
                           (STAGES > 0 ? 1 : (NW == 8 ? pick_minb(RT, MC, GM) : 2));
   const int grid = (int)(ntiles < slots ? (ntiles < 1 ? 1 : ntiles) : slots);
   ProjArgs b = a;
