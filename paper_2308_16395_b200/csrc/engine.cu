@@ -554,7 +554,7 @@ struct tsg_stream {
       double* g = dalloc(rows * rows);
       const int splits = gram_splits((int)rows, cols);
       double* part = dalloc((long long)splits * rows * rows);
-      double* work = dalloc(2 * rows * rows + 512);
+      double* work = dalloc(3 * rows * rows + 512);
       double* vec = dalloc(rows * rows);
       double* ev = dalloc(rows);
       s.owned.insert(s.owned.end(), {g, part, work, vec, ev});
@@ -573,7 +573,7 @@ struct tsg_stream {
     }
     // thin route
     double* g = dalloc(cols * cols);
-    double* work = dalloc(2 * cols * cols + 512);
+    double* work = dalloc(3 * cols * cols + 512);
     double* vec = dalloc(cols * cols);
     double* ev = dalloc(rows);
     s.owned.insert(s.owned.end(), {g, work, vec, ev});
@@ -2157,7 +2157,7 @@ int tsg_sym_eig_desc(int64_t n, const double* g, double* evals, double* evecs) {
     double* dg = s.up(g, n * n);
     double* ev = s.alloc(n);
     double* vec = s.alloc(n * n);
-    double* work = s.alloc(2 * n * n + 512);
+    double* work = s.alloc(3 * n * n + 512);
     launch_sym_eig(dg, (int)n, ev, vec, work, nullptr, s.st);
     s.down(evals, ev, n);
     s.down(evecs, vec, n * n);
@@ -2178,7 +2178,7 @@ int tsg_small_svd_truncated(int64_t m, int64_t n, const double* a, double thr, d
     double* g = s.alloc(n * n);
     double* ev = s.alloc(n);
     double* vec = s.alloc(n * n);
-    double* work = s.alloc(2 * n * n + 512);
+    double* work = s.alloc(3 * n * n + 512);
     double* rk = s.alloc(2);
     launch_gram_t(da, m, (int)n, g, s.st);
     launch_sym_eig(g, (int)n, ev, vec, work, nullptr, s.st);

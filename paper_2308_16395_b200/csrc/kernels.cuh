@@ -16,7 +16,7 @@ extern long long g_launches;  // per-process launch counter (engine copies it pe
 // in global memory, one CTA. Outputs eigenvalues (descending, clamped >= 0)
 // and eigenvectors (sign rule) exactly as sym_eig_desc (linalg.cpp:120-181)
 // specifies, with the cyclic sweep replaced by the round-robin parallel
-// ordering (every pair once per sweep). `work` holds 2 n*n doubles.
+// ordering (every pair once per sweep). `work` holds 3 n*n + 512 doubles.
 void launch_sym_eig(const double* g, int n, double* evals, double* evecs,
                     double* work, int* sweeps_out, cudaStream_t st);
 

@@ -501,8 +501,8 @@ bool launch_sym_eig_coop(const double* g, int n, double* evals, double* evecs, d
 void launch_sym_eig(const double* g, int n, double* evals, double* evecs, double* work,
                     int* sweeps_out, cudaStream_t st) {
   if (n <= 0) return;
-  // work holds 2 n^2 doubles plus room for per-CTA partials (see engine)
-  if (launch_sym_eig_coop(g, n, evals, evecs, work, work + 2LL * n * n, sweeps_out, st)) return;
+  // work holds 3 n^2 doubles plus room for per-CTA partials (see engine)
+  if (launch_sym_eig_coop(g, n, evals, evecs, work, work + 3LL * n * n, sweeps_out, st)) return;
   const size_t smem = sizeof(Rot) * ((n + 2) / 2) + sizeof(int) * (n + 1);
   static bool attr = false;
   if (!attr) {
@@ -622,12 +622,15 @@ __global__ void __launch_bounds__(256) sym_eig_coop_kernel(const double* __restr
                                                            double* evals, double* evecs,
                                                            double* work, double* part,
                                                            int* sweeps_out) {
+  // G is double-buffered (work holds G0, V, G1): a round reads G_cur and
+  // writes every entry of G_nxt, so one grid barrier per round suffices
   cg::grid_group grid = cg::this_grid();
   extern __shared__ unsigned char smem_raw[];
   RotC* rot = reinterpret_cast<RotC*>(smem_raw);
   __shared__ double red[32];
   double* G = work;
   double* V = work + (long long)n * n;
+  double* Gn = work + 2LL * n * n;
   const long long gtid = blockIdx.x * (long long)blockDim.x + threadIdx.x;
   const long long gstride = (long long)gridDim.x * blockDim.x;
   const long long nn = (long long)n * n;
@@ -653,7 +656,7 @@ __global__ void __launch_bounds__(256) sym_eig_coop_kernel(const double* __restr
       if (i != j) o2 += G[idx] * G[idx];
     }
     o2 = block_sum(o2, red);
-    grid.sync();  // everyone has read G before partials are overwritten
+    grid.sync();  // everyone has read the previous sweep's partials
     if (threadIdx.x == 0) part[blockIdx.x] = o2;
     grid.sync();
     double off = 0.0;
@@ -692,48 +695,50 @@ __global__ void __launch_bounds__(256) sym_eig_coop_kernel(const double* __restr
         }
         rot[m] = R;
       }
-      // every CTA has read the pairs' entries before any diagonal block moves
-      grid.sync();
+      __syncthreads();  // this CTA's copy of the round's rotations
       const long long nblk = (long long)half * half;
       for (long long bi = gtid; bi < nblk; bi += gstride) {
         const int m1 = (int)(bi / half), m2 = (int)(bi % half);
         if (m1 > m2) continue;
         const RotC A = rot[m1], B = rot[m2];
-        const bool idA = (A.s == 0.0 && A.t == 0.0), idB = (B.s == 0.0 && B.t == 0.0);
-        if (idA && idB) continue;
         const int p1 = A.p, q1 = A.q, p2 = B.p, q2 = B.q;
         const bool q1v = q1 < n, q2v = q2 < n;
         if (m1 == m2) {
-          const double gpq = G[p1 + (long long)q1 * n];
+          const double gpq = q1v ? G[p1 + (long long)q1 * n] : 0.0;
           const double gpp = G[p1 + (long long)p1 * n];
-          const double gqq = G[q1 + (long long)q1 * n];
-          G[p1 + (long long)p1 * n] = gpp - A.t * gpq;
-          G[q1 + (long long)q1 * n] = gqq + A.t * gpq;
-          G[p1 + (long long)q1 * n] = 0.0;
-          G[q1 + (long long)p1 * n] = 0.0;
+          const double gqq = q1v ? G[q1 + (long long)q1 * n] : 0.0;
+          const bool idA = (A.s == 0.0 && A.t == 0.0);
+          Gn[p1 + (long long)p1 * n] = idA ? gpp : gpp - A.t * gpq;
+          if (q1v) {
+            Gn[q1 + (long long)q1 * n] = idA ? gqq : gqq + A.t * gpq;
+            Gn[p1 + (long long)q1 * n] = idA ? gpq : 0.0;
+            Gn[q1 + (long long)p1 * n] = idA ? gpq : 0.0;
+          }
           continue;
         }
         const double b00 = G[p1 + (long long)p2 * n];
         const double b01 = q2v ? G[p1 + (long long)q2 * n] : 0.0;
         const double b10 = q1v ? G[q1 + (long long)p2 * n] : 0.0;
         const double b11 = (q1v && q2v) ? G[q1 + (long long)q2 * n] : 0.0;
+        // identity rotations (gpq == 0) have c = 1, s = 0: the same formulas
+        // copy the block through
         const double t00 = A.c * b00 - A.s * b10, t01 = A.c * b01 - A.s * b11;
         const double t10 = A.s * b00 + A.c * b10, t11 = A.s * b01 + A.c * b11;
         const double o00 = B.c * t00 - B.s * t01, o01 = B.s * t00 + B.c * t01;
         const double o10 = B.c * t10 - B.s * t11, o11 = B.s * t10 + B.c * t11;
-        G[p1 + (long long)p2 * n] = o00;
-        G[p2 + (long long)p1 * n] = o00;
+        Gn[p1 + (long long)p2 * n] = o00;
+        Gn[p2 + (long long)p1 * n] = o00;
         if (q2v) {
-          G[p1 + (long long)q2 * n] = o01;
-          G[q2 + (long long)p1 * n] = o01;
+          Gn[p1 + (long long)q2 * n] = o01;
+          Gn[q2 + (long long)p1 * n] = o01;
         }
         if (q1v) {
-          G[q1 + (long long)p2 * n] = o10;
-          G[p2 + (long long)q1 * n] = o10;
+          Gn[q1 + (long long)p2 * n] = o10;
+          Gn[p2 + (long long)q1 * n] = o10;
         }
         if (q1v && q2v) {
-          G[q1 + (long long)q2 * n] = o11;
-          G[q2 + (long long)q1 * n] = o11;
+          Gn[q1 + (long long)q2 * n] = o11;
+          Gn[q2 + (long long)q1 * n] = o11;
         }
       }
       for (long long idx = gtid; idx < (long long)n * half; idx += gstride) {
@@ -745,6 +750,10 @@ __global__ void __launch_bounds__(256) sym_eig_coop_kernel(const double* __restr
         V[i + (long long)R.q * n] = R.s * vp + R.c * vq;
       }
       grid.sync();
+      double* tmp = G;
+      G = Gn;
+      Gn = tmp;
+      __syncthreads();  // rot[] is rewritten next round
     }
   }
   if (blockIdx.x != 0) return;
