@@ -2106,7 +2106,10 @@ int tsg_debug_project(const double* x, int64_t left, int64_t n, int64_t right, c
     a.residual = (flags & 1) ? 0 : 1;
     a.stream_in = left == 1 ? 1 : 0;
     a.upad = up;
-    a.debug_skip = flags;
+    a.debug_skip = flags & 7;
+    // TMA mode-0 kernel profiling switches: 64 stream only; 128 / 256 / 512 skip
+    // the cross-warp reduction / phase 2 / phase 1 (results then meaningless)
+    a.karg1 = (flags & 64) ? 7 : (((flags >> 7) & 7) << 3);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);

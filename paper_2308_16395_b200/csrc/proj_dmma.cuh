@@ -497,6 +497,10 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
       if (tl < ntiles) issue(tl, (it + NS - 1) % NS);
     }
     mbar_wait(&bar[stage], (unsigned)((it / NS) & 1));
+    if (a.karg1 == 7) {  // profiling only (tools/proj0_one.py): stream the slice, no math
+      __syncthreads();
+      continue;
+    }
     const double* xt = ring + (long long)stage * BN * N;
     double X[MC][GM][2];
 #pragma unroll
@@ -535,10 +539,14 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
           for (int rt = 0; rt < RT; ++rt) dmma(acc[mc][rt][0], acc[mc][rt][1], X[mc][gi][i], b[rt]);
       }
     };
+    const int dbg = a.karg1;  // profiling only: 8 skip reduction, 16 skip phase 2, 32 skip phase 1
+    if (!(dbg & 32)) {
 #pragma unroll
-    for (int gi = 0; gi + 1 < GM; ++gi) p1(gi);
-    if (last_ok) p1(GM - 1);
+      for (int gi = 0; gi + 1 < GM; ++gi) p1(gi);
+      if (last_ok) p1(GM - 1);
+    }
     // ---- cross-warp reduction (reduce-scatter then gather; fixed order)
+    if (!(dbg & 8)) {
     double* myred = red + warp * (PER * 32);
 #pragma unroll
     for (int mc = 0; mc < MC; ++mc)
@@ -561,6 +569,9 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
       for (int rt = 0; rt < RT; ++rt)
 #pragma unroll
         for (int i = 0; i < 2; ++i) acc[mc][rt][i] = fin[((mc * RT + rt) * 2 + i) * 32 + lane];
+    } else {
+      __syncthreads();  // the ring refill relies on one barrier per tile
+    }
     // ---- store P (P[c*R + j]); each (mc, rt) block by one warp
     if (a.p) {
 #pragma unroll
@@ -580,7 +591,7 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
       }
     }
     // ---- phase 2 (all groups' DMMA chains first, then the epilogue)
-    if (a.residual) {
+    if (a.residual && !(dbg & 16)) {
       double c2[GM][MC][2];
 #pragma unroll
       for (int gi = 0; gi < GM; ++gi)
