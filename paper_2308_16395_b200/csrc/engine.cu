@@ -152,7 +152,7 @@ struct tsg_stream {
   unsigned long long* tail_clk = nullptr;  // TSG_TAIL_CLK debug stamps
   void dump_tail_clk() {
     if (!tail_clk) return;
-    std::vector<unsigned long long> h(16 * kMaxGrid);
+    std::vector<unsigned long long> h(16 * kMaxGrid + 8);
     cudaMemcpy(h.data(), tail_clk, h.size() * 8, cudaMemcpyDeviceToHost);
     unsigned long long t0 = ~0ULL;
     int nb = 0;
@@ -170,6 +170,10 @@ struct tsg_stream {
         }
       if (hi) std::fprintf(stderr, "tail stamp %2d: min %8.2f us  max %8.2f us\n", i, (lo - t0) * 1e-3, (hi - t0) * 1e-3);
     }
+    const unsigned long long* cs = h.data() + 16 * kMaxGrid;
+    if (cs[0] && cs[3])
+      std::fprintf(stderr, "tail last CTA (cycles): arrive->last %llu, reduce %llu, decide+publish %llu\n",
+                   cs[1] - cs[0], cs[2] - cs[1], cs[3] - cs[2]);
   }
   std::map<std::vector<long long>, GraphEntry> graphs;
   bool use_graphs = std::getenv("TSG_NO_GRAPH") == nullptr;
@@ -928,8 +932,8 @@ struct tsg_stream {
       ta.da = last_da[par];
       if (std::getenv("TSG_TAIL_CLK")) {
         if (!tail_clk) {
-          tail_clk = reinterpret_cast<unsigned long long*>(dalloc(16 * kMaxGrid));
-          cudaMemset(tail_clk, 0, 16 * kMaxGrid * 8);
+          tail_clk = reinterpret_cast<unsigned long long*>(dalloc(16 * kMaxGrid + 8));
+          cudaMemset(tail_clk, 0, (16 * kMaxGrid + 8) * 8);
         }
         ta.clk = tail_clk;
       }

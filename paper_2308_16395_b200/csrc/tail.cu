@@ -182,16 +182,23 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs t) {
   if (!last) return;
   cstamp(1);
   __threadfence();
-  if (threadIdx.x == 0) {
-    for (int k = a.first_mode; k < t.m0; ++k) res[k] = __ldcg(t.part + (long long)kMaxD * gridDim.x + k);
-    if (a.first_mode == 0 && t.m0 > 0) xsq = __ldcg(t.part + (long long)kMaxD * gridDim.x + kMaxD);
-  }
-  for (int k = t.m0; k < t.m1; ++k) {
-    double acc = 0.0;
-    for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x)
-      acc += __ldcg(t.part + (long long)k * gridDim.x + b);
-    acc = block_sum(acc, red);
-    if (threadIdx.x == 0) res[k] = acc;
+  // one warp per tail mode reduces that mode's per-CTA partials (all loads in
+  // flight at once, fixed lane order); the last warp fetches the leading
+  // modes' sums. No block-wide barrier before the decision.
+  {
+    const int nm = t.m1 - t.m0;
+    const unsigned g = gridDim.x;
+    if (wid < nm) {
+      const int k = t.m0 + wid;
+      const double* pk = t.part + (long long)k * g;
+      double acc = 0.0;
+      for (unsigned b = lane; b < g; b += 32) acc += __ldcg(pk + b);
+      acc = warp_sum(acc);
+      if (lane == 0) res[k] = acc;
+    } else if (wid == nm && lane == 0) {
+      for (int k = a.first_mode; k < t.m0; ++k) res[k] = __ldcg(t.part + (long long)kMaxD * g + k);
+      if (a.first_mode == 0 && t.m0 > 0) xsq = __ldcg(t.part + (long long)kMaxD * g + kMaxD);
+    }
   }
   __syncthreads();
   cstamp(2);
