@@ -13,9 +13,23 @@ if name in ("c2", "c3", "c5"):
     case = cases.config_case(cfg, n_slices=cfg.n_init + 8)
 else:
     case = cases.STREAM_CASES[name]()
-st = S.stream_init(case.init_flat, case.tau, dims=case.init_dims)
-for s in case.slices[:8]:
-    st.stream_update(s)
+asyn = bool(os.environ.get("ASYNC"))
+if asyn and name in ("c2", "c3", "c5"):
+    # device-resident slices through the async engine (the insertion overlaps
+    # the next slices' projections): clocks of the last insertion
+    import torch
+    dev = torch.device("cuda", 0)
+    gen = dg.make_stream(cfg)
+    st = S.StreamingState(device=0, asynchronous=True)
+    st.init_flat(torch.as_tensor(case.init_flat, device=dev), case.init_dims, case.tau)
+    ys = [gen.slice_torch(cfg.n_init + i, dev) for i in range(30)]
+    for y in ys:
+        st.stream_update(y)
+    st.synchronize()
+else:
+    st = S.stream_init(case.init_flat, case.tau, dims=case.init_dims)
+    for s in case.slices[:8]:
+        st.stream_update(s)
 c = np.zeros(32, dtype=np.int64)
 L.tsg_debug_isvd_clocks(c.ctypes.data_as(ctypes.c_void_p))
 print(name, st.query()["core_dims"], "pgram", c[8] - c[0], "passes", c[1] - c[8], "pre", c[4] - c[1],
