@@ -274,3 +274,30 @@ def test_nccl_transport_world1_matches_loopback(tmp_path):
     np.testing.assert_array_equal(z["core"], ref.core)
     np.testing.assert_array_equal(z["left"], ref.left)
     assert int(z["exchanges"]) >= len(case.slices)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_loopback_sharded_config4_vs_oracle(oracle):
+    """Config-4 generator (5-way, 48^3 x 16): the variable mode (16 rows) is
+    the sharded mode, modes 0-2 are local and grow on most slices, so the
+    growth-at-a-local-mode exchange (gather of that mode's input) runs every
+    few slices. Ranks bitwise identical, state within the parity bounds."""
+    _need_gpu()
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.scaled(dg.CONFIGS["c4"], (48, 48, 48, 16), n_slices=15, n_init=10, name="c4_48s")
+    case = cases.config_case(cfg)
+    states = _run_loopback(case, 2)
+    a, b = states[0].export(), states[1].export()
+    np.testing.assert_array_equal(a.core, b.core)
+    np.testing.assert_array_equal(a.left, b.left)
+    x = case.init_flat.reshape(case.init_dims[::-1]).transpose()
+    ho = oracle.stream_init(x, case.tau)
+    for y in case.slices:
+        ho.update_flat(y)
+    so = ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(states[0].metrics(), a.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(a, so)
+    print("c4 sharded", mc, sc)
+    P.assert_parity(mc, sc, resid_tol=5e-8)
