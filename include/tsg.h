@@ -201,6 +201,10 @@ double* tsg_slice_buffer(tsg_stream* h, int32_t which);
  * ms, out[3] = ISVD + core rotation ms, out[4] = host gap ms (decision
  * readback), out[5] = mode-0 kernel launches. n >= 6. Resets when reset != 0. */
 int tsg_profile(tsg_stream* h, double* out, int32_t n, int32_t reset);
+/* Per-slice timeline (TSG_PROFILE, since the last tsg_profile reset): five
+ * times in ms per profiled slice — mode-0 start, mode-0 end, decision (tail
+ * end), insertion start, insertion end. Returns the rows written, -1 on error. */
+int64_t tsg_profile_timeline(tsg_stream* h, double* out, int64_t cap);
 /* FP64 pipe peaks on a device, TFLOP/s: DMMA (mma.sync f64) and DFMA. */
 int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tflops);
 

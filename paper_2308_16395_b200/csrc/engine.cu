@@ -300,6 +300,21 @@ struct tsg_stream {
     prof[3] += c;
     prof[4] += g;
     prof[5] += 1;
+    if (tl_base && timeline.size() < 100000) {
+      std::array<float, 5> row{};
+      for (int i = 0; i < 5; ++i) cudaEventElapsedTime(&row[i], tl_base, pev[q][i]);
+      timeline.push_back(row);
+    }
+  }
+  // per-slice timeline (TSG_PROFILE): event times of mode-0 start / end, tail
+  // end (decision), insertion start / end, relative to the last profile reset
+  cudaEvent_t tl_base = nullptr;
+  std::vector<std::array<float, 5>> timeline;
+  void reset_timeline() {
+    if (!tl_base) ck(cudaEventCreate(&tl_base), "event");
+    ck(cudaEventRecord(tl_base, st), "cudaEventRecord");
+    ck(cudaEventSynchronize(tl_base), "cudaEventSynchronize");
+    timeline.clear();
   }
   void resolve_all() {
     for (int q = 0; q < kProfSets; ++q) resolve_prof(q);
@@ -393,6 +408,14 @@ struct tsg_stream {
   static constexpr long long kPartStride = kTailPart + (long long)kMaxD * kMaxGrid + 64;
   DecideArgs last_da[kNP];  // partial layout of the last captured leading-mode pass
   bool use_tail = std::getenv("TSG_NO_TAIL") == nullptr;
+  // Mode-0 slice loads carry an L2 evict-first hint: the insertion chain
+  // (the slice period's bound) then keeps Q, core and the streaming factor in
+  // L2 while the next slices stream through (C2: insertion 58 -> 52 us,
+  // 15.5 k -> 17.1 k slices/s, same-box A/B). TSG_EVICT_FIRST=0 disables.
+  bool evict_first = [] {
+    const char* e = std::getenv("TSG_EVICT_FIRST");
+    return e ? std::atoi(e) != 0 : true;
+  }();
   // First mode handled by the fused tail kernel (d-1: none; the tail then
   // only decides): trailing modes with small inputs.
   int tail_start() const {
@@ -630,7 +653,7 @@ struct tsg_stream {
     a.e = e;
     a.partial = part;
     a.residual = 1;
-    a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? 1 : 0;
+    a.stream_in = (mode == 0 && y != w0 && y != w1 && y != w2) ? (evict_first ? 2 : 1) : 0;
     prep_proj(mode);
     a.upad = upad[mode];
     if (shard_world > 0) {
@@ -2073,9 +2096,25 @@ int tsg_profile(tsg_stream* h, double* out, int32_t n, int32_t reset) {
     h->sync();
     h->resolve_all();
     for (int i = 0; i < n && i < 6; ++i) out[i] = h->prof[i];
-    if (reset)
+    if (reset) {
       for (double& v : h->prof) v = 0.0;
+      if (h->profiling()) h->reset_timeline();
+    }
   });
+}
+
+int64_t tsg_profile_timeline(tsg_stream* h, double* out, int64_t cap) {
+  int64_t n = 0;
+  const int st = guarded(h, [&] {
+    h->sync();
+    h->resolve_all();
+    for (const auto& row : h->timeline) {
+      if (n >= cap) break;
+      for (int i = 0; i < 5; ++i) out[5 * n + i] = row[i];
+      ++n;
+    }
+  });
+  return st == TSG_OK ? n : -1;
 }
 
 int tsg_measure_fp64_peaks(int32_t device, double* dmma_tflops, double* dfma_tflops) {

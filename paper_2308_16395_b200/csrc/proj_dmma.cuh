@@ -82,6 +82,22 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Same copy with an L2 evict-first policy: a slice streamed once should not
+// push the small hot state the insertion kernel reads (Q, core, the streaming
+// factor) out of L2.
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_ef(void* dst, const void* src, unsigned bytes,
+                                            unsigned long long* bar, unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
   asm volatile(
       "{\n"
@@ -463,12 +479,17 @@ __global__ void __launch_bounds__(256, MINB) proj0_tma_kernel(ProjArgs a) {
   const int g = lane >> 2, t = lane & 3;
   const long long ntiles = (cols + BN - 1) / BN;
   const double* xsrc = a.x;
+  const bool ef = a.stream_in == 2;  // slice read exactly once: evict-first in L2
+  const unsigned long long pol = ef ? l2_evict_first_policy() : 0ull;
   auto issue = [&](long long tl, int stage) {
     const long long c0 = tl * BN;
     const long long nc = (cols - c0) < BN ? (cols - c0) : BN;
     const unsigned bytes = (unsigned)(nc * N * 8);
     mbar_expect_tx(&bar[stage], bytes);
-    bulk_g2s(ring + (long long)stage * BN * N, xsrc + c0 * N, bytes, &bar[stage]);
+    if (ef)
+      bulk_g2s_ef(ring + (long long)stage * BN * N, xsrc + c0 * N, bytes, &bar[stage], pol);
+    else
+      bulk_g2s(ring + (long long)stage * BN * N, xsrc + c0 * N, bytes, &bar[stage]);
   };
   if (threadIdx.x == 0) {
     for (int s_ = 0; s_ < NS; ++s_) mbar_init(&bar[s_], 1);

@@ -101,7 +101,7 @@ EXPORTED = [
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
     "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
     "tsg_shard_setup", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
-    "tsg_error_sums",
+    "tsg_error_sums", "tsg_profile_timeline",
 ]
 
 _LIB = None
@@ -154,6 +154,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.tsg_shard_setup.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _i64p]
     L.tsg_shard_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TsgExchange)]
     L.tsg_shard_continue.argtypes = [C.c_void_p, C.POINTER(TsgExchange)]
+    L.tsg_profile_timeline.argtypes = [C.c_void_p, _dp, C.c_int64]
+    L.tsg_profile_timeline.restype = C.c_int64
     L.tsg_reconstruct.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_int32]
     L.tsg_error_sums.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int32, _dp, _dp]
     _LIB = L
@@ -360,6 +362,15 @@ class StreamingState:
         n = max(out[0], 1.0)
         return {"updates": int(out[0]), "mode0_ms": out[1] / n, "rest_proj_ms": out[2] / n,
                 "isvd_ms": out[3] / n, "host_gap_ms": out[4] / n}
+
+    def timeline(self, cap: int = 4096) -> np.ndarray:
+        """(slices x 5) ms: mode-0 start, mode-0 end, decision, insertion
+        start, insertion end of the profiled slices since the last reset."""
+        out = np.zeros(5 * cap)
+        n = int(self.L.tsg_profile_timeline(self.h, _p(out), cap))
+        if n < 0:
+            self._check(4)
+        return out[: 5 * n].reshape(n, 5)
 
     def kernel_launches(self) -> int:
         return int(self.L.tsg_kernel_launches(self.h))
