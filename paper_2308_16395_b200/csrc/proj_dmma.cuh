@@ -32,14 +32,6 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
                : "d"(a), "d"(b));
 }
 
-// Same instruction without `volatile`, so the compiler may interleave
-// independent accumulator chains (the result is always consumed).
-__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
-      : "+d"(c0), "+d"(c1)
-      : "d"(a), "d"(b));
-}
-
 template <int RT, int MC, int NW = 8>
 constexpr int red_doubles() {
   return (NW + 1) * MC * RT * 2 * 32;  // NW warp partials + the reduced copy
@@ -735,290 +727,10 @@ inline int launch0_rt(const ProjArgs& a, cudaStream_t st) {
   return a.e ? launch0_t<RT, MC, GM, true, 1>(a, st) : launch0_t<RT, MC, GM, false, 1>(a, st);
 }
 
-// ---------------------------------------------------------------------------
-// Mode-0 projection, warp-owned column tiles ("proj0w"). Each of the 4 warps
-// of a CTA (one per SM sub-partition, one CTA per SM) streams its own 8-column
-// tiles (8 x N doubles, contiguous) through a private NS-stage ring filled by
-// one bulk copy (TMA) per tile and an mbarrier per stage, so no CTA-wide
-// barrier exists in the steady state and the whole fibre is in one warp:
-//   phase 1  P^T (8 x R) = X^T U over all N rows (K = N), two accumulator
-//            chains per rank tile (even / odd row octets) -> no cross-warp sum;
-//   phase 2  Rec^T (8 x N) = P^T U^T with K = R rounded up to 4 (not 8): the
-//            rank columns are permuted (image column 8rt + 2t + i holds rank
-//            8rt + 4i + t) so a phase-1 accumulator pair covers two K-steps of
-//            four consecutive ranks and K-steps beyond R are skipped;
-//   epilogue E = X - Rec from the staged tile, ||E||^2, ||X||^2 (and E).
-// U is staged once per CTA, row-major with pitch 8 RT + 4 (conflict-free
-// fragment loads). DMMA per 8 columns: N/4 RT + (N/8) ceil(R/4).
-template <int RT, int KS, bool WE>
-__global__ void __launch_bounds__(128, 1) proj0w_kernel(ProjArgs a) {
-  constexpr int RP = 8 * RT + 4;  // phase-1 image pitch (row-major, permuted rank columns)
-  const int NS = a.karg0;
-  const int N = (int)a.v.n;  // even
-  const long long cols = a.v.right;
-  const int R = a.R;
-  const int ng = (N + 7) >> 3;   // row octets
-  const int N8 = ng * 8;
-  const int CP = N8 + 4;         // phase-2 image pitch (rank-major, rows contiguous)
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ double sred[32];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int g = lane >> 2, t = lane & 3;
-  double* Us = reinterpret_cast<double*>(smraw);                   // N8 x RP
-  double* Vs = Us + (long long)N8 * RP;                            // 4 KS x CP
-  double* ring = Vs + (long long)4 * KS * CP;                      // [4][NS][8 N8]
-  unsigned long long* bar = reinterpret_cast<unsigned long long*>(ring + 4LL * NS * 8 * N8);
-  double* wring = ring + (long long)warp * NS * 8 * N8;
-  unsigned long long* wbar = bar + warp * NS;
-  const long long ntiles = (cols + 7) >> 3;
-  const long long stride = (long long)gridDim.x * 4;
-  const long long first = (long long)blockIdx.x * 4 + warp;
-  const double* xsrc = a.x;
-  auto issue = [&](long long tl, int s) {
-    const long long c0 = tl * 8;
-    const long long nc = (cols - c0) < 8 ? (cols - c0) : 8;
-    const unsigned bytes = (unsigned)(nc * N * 8);
-    mbar_expect_tx(&wbar[s], bytes);
-    bulk_g2s(wring + (long long)s * 8 * N8, xsrc + c0 * N, bytes, &wbar[s]);
-  };
-  // Rows N..N8-1 of the last column of a stage read the stage tail (zeroed
-  // once; the TMA never writes it) against zero U rows. Columns beyond a short
-  // last tile only feed their own (discarded) output rows.
-  if (N8 > N)
-    for (int i = threadIdx.x; i < 4 * NS * 8 * (N8 - N); i += 128) {
-      const int st_ = i / (8 * (N8 - N)), o = i - st_ * 8 * (N8 - N);
-      ring[(long long)st_ * 8 * N8 + 8 * N + o] = 0.0;
-    }
-  // phase-1 image: Us[row][8rt + 2t + i] = U[row][8rt + 4i + t]
-  for (int i = threadIdx.x; i < N8 * RP; i += 128) {
-    const int row = i / RP, c = i - row * RP;
-    const int rk = c < 8 * RT ? (c & ~7) + 4 * (c & 1) + ((c & 7) >> 1) : R;
-    Us[i] = (row < N && rk < R) ? __ldg(a.u + row + (long long)rk * N) : 0.0;
-  }
-  // phase-2 image: Vs[rank][row] (rank-major)
-  for (int i = threadIdx.x; i < 4 * KS * CP; i += 128) {
-    const int rk = i / CP, row = i - rk * CP;
-    Vs[i] = (row < N && rk < R) ? __ldg(a.u + row + (long long)rk * N) : 0.0;
-  }
-  if (threadIdx.x < 4 * NS) mbar_init(&bar[threadIdx.x], 1);
-  mbar_fence_init();
-  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  __syncthreads();
-  if (lane == 0)
-    for (int s = 0; s < NS - 1; ++s) {
-      const long long tl = first + (long long)s * stride;
-      if (tl < ntiles) issue(tl, s);
-    }
-  double racc = 0.0, xacc = 0.0;
-  int it = 0;
-#pragma unroll 1
-  for (long long tile = first; tile < ntiles; tile += stride, ++it) {
-    const int s = it % NS;
-    if (lane == 0) {
-      const long long tl = tile + (long long)(NS - 1) * stride;
-      if (tl < ntiles) issue(tl, (it + NS - 1) % NS);
-    }
-    mbar_wait(&wbar[s], (unsigned)((it / NS) & 1));
-    const double* xt = wring + (long long)s * 8 * N8 + g * N;  // this lane's column
-    // ---- phase 1: two octets per step into two accumulator sets; dependent
-    // DMMAs sit 2 RT instructions apart (volatile asm keeps this order), the
-    // next step's operands are loaded before this step's DMMAs
-    const double* up = Us + (2 * t) * RP + g;
-    double acc[2][RT][2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-      for (int rt = 0; rt < RT; ++rt) acc[h][rt][0] = acc[h][rt][1] = 0.0;
-    struct Ops {
-      double2 xv[2];
-      double b0[2][RT], b1[2][RT];
-    };
-    auto load = [&](int q, Ops& o) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int qq = q + h < ng ? q + h : ng - 1;  // clamped (an odd tail feeds zeros below)
-        o.xv[h] = *reinterpret_cast<const double2*>(xt + 8 * qq + 2 * t);
-        const double* uq = up + (8 * qq) * RP;
-#pragma unroll
-        for (int rt = 0; rt < RT; ++rt) {
-          o.b0[h][rt] = uq[8 * rt];
-          o.b1[h][rt] = uq[RP + 8 * rt];
-        }
-      }
-    };
-    auto compute = [&](const Ops& o, int nh) {
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int rt = 0; rt < RT; ++rt)
-          dmma(acc[h][rt][0], acc[h][rt][1], h < nh ? o.xv[h].x : 0.0, o.b0[h][rt]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int rt = 0; rt < RT; ++rt)
-          dmma(acc[h][rt][0], acc[h][rt][1], h < nh ? o.xv[h].y : 0.0, o.b1[h][rt]);
-    };
-    {
-      Ops cur, nxt;
-      load(0, cur);
-      int q = 0;
-#pragma unroll 1
-      for (; q + 2 < ng; q += 2) {
-        load(q + 2, nxt);
-        compute(cur, 2);
-        cur = nxt;
-      }
-      compute(cur, ng - q);  // last one or two octets
-    }
-    double pv[RT][2];
-#pragma unroll
-    for (int rt = 0; rt < RT; ++rt)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) pv[rt][i] = acc[0][rt][i] + acc[1][rt][i];
-    const long long c = tile * 8 + g;
-    const bool cv = c < cols;
-    if (a.p && cv) {
-#pragma unroll
-      for (int rt = 0; rt < RT; ++rt)
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const int j = 8 * rt + 4 * i + t;
-          if (j < R) a.p[c * R + j] = pv[rt][i];
-        }
-    }
-    // ---- phase 2 + epilogue, NB row octets at a time (NB independent chains
-    // of KS DMMAs); K-step k covers ranks 4k..4k+3 = accumulator pv[k/2][k%2]
-    if (a.residual) {
-      constexpr int NB = 4;
-      const double* vb = Vs + (long long)t * CP + g;  // Vs[4k + t][8 nt + g]
-      auto loadb = [&](int n0, double (&bv)[KS][NB]) {
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int nt = n0 + j < ng ? n0 + j : ng - 1;
-#pragma unroll
-          for (int k = 0; k < KS; ++k) bv[k][j] = vb[(4 * k) * CP + 8 * nt];
-        }
-      };
-      auto block = [&](int n0, int nb, const double (&bv)[KS][NB]) {
-        double cc[NB][2];
-        double2 xv[NB];
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          cc[j][0] = cc[j][1] = 0.0;
-          const int nt = n0 + j < ng ? n0 + j : ng - 1;
-          xv[j] = *reinterpret_cast<const double2*>(xt + 8 * nt + 2 * t);
-        }
-#pragma unroll
-        for (int k = 0; k < KS; ++k)
-#pragma unroll
-          for (int j = 0; j < NB; ++j) dmma(cc[j][0], cc[j][1], pv[k >> 1][k & 1], bv[k][j]);
-#pragma unroll
-        for (int j = 0; j < NB; ++j) {
-          const int row = 8 * (n0 + j) + 2 * t;
-          if (j < nb && cv && row < N) {
-            const double e0 = xv[j].x - cc[j][0], e1 = xv[j].y - cc[j][1];
-            racc = fma(e0, e0, racc);
-            racc = fma(e1, e1, racc);
-            xacc = fma(xv[j].x, xv[j].x, xacc);
-            xacc = fma(xv[j].y, xv[j].y, xacc);
-            if constexpr (WE) {
-              a.e[c * N + row] = e0;
-              a.e[c * N + row + 1] = e1;
-            }
-          }
-        }
-      };
-      double bcur[KS][NB], bnxt[KS][NB];
-      loadb(0, bcur);
-      int n0 = 0;
-#pragma unroll 1
-      for (; n0 + NB < ng; n0 += NB) {
-        loadb(n0 + NB, bnxt);
-        block(n0, NB, bcur);
-#pragma unroll
-        for (int k = 0; k < KS; ++k)
-#pragma unroll
-          for (int j = 0; j < NB; ++j) bcur[k][j] = bnxt[k][j];
-      }
-      block(n0, ng - n0, bcur);
-    }
-    // the stage is refilled next iteration: every lane's reads are done
-    __syncwarp();
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  }
-  racc = block_sum(racc, sred);
-  xacc = block_sum(xacc, sred);
-  if (threadIdx.x == 0 && a.partial) {
-    a.partial[2 * blockIdx.x] = racc;
-    a.partial[2 * blockIdx.x + 1] = xacc;
-  }
-}
-
-template <int RT, int KS, bool WE>
-inline int launch0w_t(const ProjArgs& a, cudaStream_t st) {
-  const long long N = a.v.n;
-  const long long N8 = (N + 7) / 8 * 8;
-  const long long ubytes = N8 * (8 * RT + 4) * 8 + 4LL * KS * (N8 + 4) * 8;
-  const long long stage = 8 * N8 * 8;
-  const long long cap = 225 * 1024;
-  int NS = 4;
-  while (NS >= 2 && ubytes + 4 * NS * stage + 8 * 4 * NS > cap) --NS;
-  if (NS < 2) return -1;
-  const size_t smem = (size_t)(ubytes + 4 * NS * stage + 8 * 4 * NS);
-  static size_t attr = 0;
-  if (smem > attr) {
-    if (cudaFuncSetAttribute(proj0w_kernel<RT, KS, WE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)cap) != cudaSuccess)
-      return -1;
-    attr = cap;
-  }
-  const long long ntiles = (a.v.right + 7) / 8;
-  static const long long cap_ctas = [] {
-    const char* e = std::getenv("TSG_M0_CTAS");
-    return e ? std::atoll(e) : 0LL;
-  }();
-  long long grid = kNumSMs - 8;  // room for the overlapping tail / insertion kernels
-  if (cap_ctas > 0) grid = cap_ctas;
-  const long long need = (ntiles + 3) / 4;
-  if (need < grid) grid = need < 1 ? 1 : need;
-  ProjArgs b = a;
-  b.karg0 = NS;
-  proj0w_kernel<RT, KS, WE><<<(int)grid, 128, smem, st>>>(b);
-  return (int)grid;
-}
-
-template <int RT, int KS>
-inline int launch0w_k(const ProjArgs& a, cudaStream_t st) {
-  return a.e ? launch0w_t<RT, KS, true>(a, st) : launch0w_t<RT, KS, false>(a, st);
-}
-
-inline int launch0w(const ProjArgs& a, cudaStream_t st) {
-  static const int off = [] {  // opt-in (TSG_PROJ0W=1): one warp per SM sub-partition
-    const char* e = std::getenv("TSG_PROJ0W");
-    return e ? (std::atoi(e) == 0) : 1;
-  }();
-  if (off) return -1;
-  switch ((a.R + 3) / 4) {
-    case 1: return launch0w_k<1, 1>(a, st);
-    case 2: return launch0w_k<1, 2>(a, st);
-    case 3: return launch0w_k<2, 3>(a, st);
-    case 4: return launch0w_k<2, 4>(a, st);
-    case 5: return launch0w_k<3, 5>(a, st);
-    case 6: return launch0w_k<3, 6>(a, st);
-    case 7: return launch0w_k<4, 7>(a, st);
-    case 8: return launch0w_k<4, 8>(a, st);
-  }
-  return -1;
-}
-
 inline int launch0(const ProjArgs& a, cudaStream_t st) {
   const long long N = a.v.n;
   if (a.v.left != 1 || (N & 1) || N > 256 || a.R > 32 || a.R < 1 || !a.upad) return -1;
   if (a.v.right >= (1LL << 31)) return -1;
-  {
-    const int g = launch0w(a, st);
-    if (g > 0) return g;
-  }
   const int ngroups = (int)((N + 7) / 8);
   const int RT = (a.R + 7) / 8;
   if (ngroups <= 8) {
