@@ -120,6 +120,7 @@ __global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
       }
       block_reduce_vec<RMAX, true, NW>(acc, wp, sp1);
     }
+    double e1sq = 0.0;
     {
       double acc[RMAX];
 #pragma unroll
@@ -132,32 +133,31 @@ __global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
           pr[l] = qq[l] * sp1[l];
         }
         const double e1 = B.b[i] - tree_sum<RMAX>(pr);
-        se1[i] = e1;
+        e1sq = fma(e1, e1, e1sq);
 #pragma unroll
         for (int l = 0; l < RMAX; ++l) acc[l] = fma(qq[l], e1, acc[l]);
       }
       block_reduce_vec<RMAX, true, NW>(acc, wp, sp2);
     }
     {
-      double es = 0.0;
-      for (long long i = tid; i < n; i += 256) {
-        double pr[RMAX];
-#pragma unroll
-        for (int l = 0; l < RMAX; ++l) pr[l] = (l < r ? B.q[i + (long long)l * n] : 0.0) * sp2[l];
-        const double e = se1[i] - tree_sum<RMAX>(pr);
-        es = fma(e, e, es);
-      }
-      double ev[2] = {es, bsq_part};
+      // ||e||^2 for e = e1 - Q p2 without a third pass over the rows:
+      // ||e1||^2 - 2 p2^T Q^T e1 + ||Q p2||^2 = ||e1||^2 - ||p2||^2 up to
+      // terms of order ||p2||^2 (Q^T Q - I), i.e. ~1e-24 ||b||^2: p2 is the
+      // reorthogonalisation correction, ~eps ||b||
+      double ev[2] = {e1sq, bsq_part};
       block_reduce_vec<2, false, NW>(ev, wp, red);
     }
     TSG_CLK(1);
     if (tid < RMAX) sp[tid] = sp1[tid] + sp2[tid];
     if (tid == 0) {
+      double p2sq = 0.0;
+      for (int l = 0; l < r; ++l) p2sq = fma(sp2[l], sp2[l], p2sq);
+      const double esq = fmax(red[0] - p2sq, 0.0);
       sh_bsq = red[1];
-      sh_esq = red[0];
+      sh_esq = esq;
       c->proj_sq = red[1];
-      c->e_sq = red[0];
-      sh_deg = (sqrt(red[0]) <= kOrthEps * sqrt(red[1])) ? 1 : 0;  // isvd.cpp:191
+      c->e_sq = esq;
+      sh_deg = (sqrt(esq) <= kOrthEps * sqrt(red[1])) ? 1 : 0;  // isvd.cpp:191
     }
     if (tid < 32) ssig[tid] = tid < r ? B.sigma[tid] : 0.0;
     __syncthreads();
