@@ -70,7 +70,10 @@ enum tsg_flags {
    * surface at the next call. Default: synchronous, like the reference. */
   TSG_ASYNC = 1,
   /* Record CUDA events around the update phases (read with tsg_profile). */
-  TSG_PROFILE = 2
+  TSG_PROFILE = 2,
+  /* Only the mode-0 projection kernel's events (its duration for roofline
+   * accounting) — no event nodes on the tail / insertion streams. */
+  TSG_PROFILE_MODE0 = 4
 };
 
 typedef struct tsg_stream tsg_stream;

@@ -280,14 +280,27 @@ struct tsg_stream {
   bool pev_live[kProfSets] = {};
   int cur_q = -1;  // event set of the slice being enqueued (-1: none)
   double prof[6] = {0, 0, 0, 0, 0, 0};
-  bool profiling() const { return flags & TSG_PROFILE; }
+  bool profiling() const { return flags & (TSG_PROFILE | TSG_PROFILE_MODE0); }
+  // TSG_PROFILE_MODE0: only the mode-0 kernel's events (stream st); the
+  // tail / insertion streams — the slice period's critical path — carry none
+  bool prof_m0_only() const { return !(flags & TSG_PROFILE); }
   void ev_mark(int i, cudaStream_t s_, bool cap) {
     if (!profiling() || cur_q < 0) return;
+    if (prof_m0_only() && i > 1) return;
     record_ev(pev[cur_q][i], s_, cap);
   }
   void resolve_prof(int q) {
     if (!pev_live[q]) return;
     pev_live[q] = false;
+    if (prof_m0_only()) {
+      ck(cudaEventSynchronize(pev[q][1]), "cudaEventSynchronize");
+      float a = 0.f;
+      cudaEventElapsedTime(&a, pev[q][0], pev[q][1]);
+      prof[0] += 1;
+      prof[1] += a;
+      prof[5] += 1;
+      return;
+    }
     ck(cudaEventSynchronize(pev[q][4]), "cudaEventSynchronize");
     float a = 0.f, b = 0.f, c = 0.f, g = 0.f;
     cudaEventElapsedTime(&a, pev[q][0], pev[q][1]);
@@ -843,7 +856,7 @@ struct tsg_stream {
                                     (long long)(uintptr_t)evec, (long long)(uintptr_t)pgram,
                                     (long long)(uintptr_t)inner, (long long)(uintptr_t)ipart,
                                     (long long)(uintptr_t)isvd_hand, (long long)(uintptr_t)isvd_gsync,
-                                    n, cap_rows, capr, B.r_hint, d, q};
+                                    n, cap_rows, capr, B.r_hint, d, prof_m0_only() ? -1 : q};
       for (int k = 0; k + 1 < d; ++k) key.push_back(R[k]);
       run(key, s_, body);
     } else {

@@ -29,7 +29,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libtsg.so")
 MAXD = 8
 MEM_HOST, MEM_DEVICE = 0, 1
-ASYNC, PROFILE = 1, 2
+ASYNC, PROFILE, PROFILE_MODE0 = 1, 2, 4
 
 _i64p = C.POINTER(C.c_int64)
 _dp = C.POINTER(C.c_double)
@@ -219,9 +219,11 @@ class StreamingState:
     """Owns one device-resident streaming state (a tsg_stream handle)."""
 
     def __init__(self, device: int = 0, asynchronous: bool = False, rank_capacity: int = 0,
-                 row_capacity: int = 0, profile: bool = False):
+                 row_capacity: int = 0, profile: bool | str = False):
+        """profile: False, True (all phases) or "mode0" (the mode-0 kernel only)."""
         self.L = load_library()
-        flags = (ASYNC if asynchronous else 0) | (PROFILE if profile else 0)
+        prof = PROFILE_MODE0 if profile == "mode0" else (PROFILE if profile else 0)
+        flags = (ASYNC if asynchronous else 0) | prof
         cfg = TsgConfig(device, flags, rank_capacity, row_capacity, 0)
         h = C.c_void_p()
         code = self.L.tsg_create(C.byref(cfg), C.byref(h))
