@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
     g_isvd_clk[24] = (long long)g;
   }
   if (tid == 0) {
-    sh_epoch = *reinterpret_cast<volatile unsigned*>(gs);
+    sh_epoch = __ldcg(gs);  // written by the previous launch (kernel boundary)
     sh_r = c->r;    // c->r and c->n_d change only in the final record (this kernel's end)
     sh_nd = c->n_d;
     if (leader) {
@@ -88,20 +88,37 @@ __global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
       sh_sqerr = c->squared_error;
     }
   }
+  if (leader) TSG_CLK(21);
   __syncthreads();
+  if (leader) TSG_CLK(22);
   const int r = sh_r;
   const long long n_d = sh_nd;
   const unsigned epoch = sh_epoch;
   // this CTA's rows, prefetched before any waiting
   const long long row = (long long)blockIdx.x * kGridRows + tid;
   const bool has_row = tid < kGridRows && row < n;
-  double qv[RMAX], cv[RMAX], bvr = 0.0;
+  // all loads unconditional from clamped (valid, written) addresses so they
+  // issue back to back; out-of-range entries are zeroed by a 0/1 factor
+  // (a predicated load followed by a zeroing move serialises on the register)
+  double qv[RMAX], cv[RMAX], bvr;
+  {
+    const long long rowc = has_row ? row : 0;
+    double mk[RMAX];
 #pragma unroll
-  for (int l = 0; l < RMAX; ++l) {
-    qv[l] = (has_row && l < r) ? B.q[row + (long long)l * n] : 0.0;
-    cv[l] = (has_row && l < r) ? B.c[row + (long long)l * n] : 0.0;
+    for (int l = 0; l < RMAX; ++l) {
+      const long long idx = rowc + (long long)(l < r ? l : 0) * n;
+      qv[l] = B.q[idx];
+      cv[l] = B.c[idx];
+      mk[l] = (has_row && l < r) ? 1.0 : 0.0;
+    }
+    bvr = B.b[rowc];
+#pragma unroll
+    for (int l = 0; l < RMAX; ++l) {
+      qv[l] *= mk[l];
+      cv[l] *= mk[l];
+    }
+    if (!has_row) bvr = 0.0;
   }
-  if (has_row) bvr = B.b[row];
   if (leader) {
     TSG_CLK(8);
     // ---- CGS2 over all rows (isvd.cpp:172-191), same arithmetic per row as

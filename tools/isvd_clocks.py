@@ -44,4 +44,5 @@ print("update rows", c[14] - c[2], "left", c[15] - c[14], "reduce", c[3] - c[15]
 print("M+sw", c[16] - c[2], "wait+sync", c[17] - c[16], "row0", c[18] - c[17], "row1", c[14] - c[18])
 print("grid leader: M+inv", c[16] - c[2], "handoff", c[17] - c[16], "own rows", c[18] - c[17], "left", c[14] - c[18], "reduce+publish", c[9] - c[14])
 print("own rows: e", c[19] - c[17], "chunk0", c[20] - c[19], "chunk1", c[18] - c[20])
+print("prologue: ctrl/slot/commit %d, barrier %d, prefetch issue %d" % (c[21] - c[0], c[22] - c[21], c[8] - c[22]))
 print("grid kernel wall (leader entry -> last CTA publish): %.2f us" % ((c[25] - c[24]) * 1e-3))
