@@ -124,15 +124,26 @@ __global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
     // ---- CGS2 over all rows (isvd.cpp:172-191), same arithmetic per row as
     // the followers' recomputation below
     double bsq_part = 0.0;
+    // Q columns l >= r are read from column 0 and zeroed by a 0/1 factor:
+    // unconditional loads issue back to back (see the row prefetch above)
+    double mk[RMAX];
+    long long coff[RMAX];
+#pragma unroll
+    for (int l = 0; l < RMAX; ++l) {
+      mk[l] = l < r ? 1.0 : 0.0;
+      coff[l] = (long long)(l < r ? l : 0) * n;
+    }
     {
       double acc[RMAX];
 #pragma unroll
       for (int l = 0; l < RMAX; ++l) acc[l] = 0.0;
       for (long long i = tid; i < n; i += 256) {
         const double bi = B.b[i];
+        double qq[RMAX];
 #pragma unroll
-        for (int l = 0; l < RMAX; ++l)
-          if (l < r) acc[l] = fma(B.q[i + (long long)l * n], bi, acc[l]);
+        for (int l = 0; l < RMAX; ++l) qq[l] = B.q[i + coff[l]];
+#pragma unroll
+        for (int l = 0; l < RMAX; ++l) acc[l] = fma(qq[l] * mk[l], bi, acc[l]);
         bsq_part = fma(bi, bi, bsq_part);
       }
       block_reduce_vec<RMAX, true, NW>(acc, wp, sp1);
@@ -145,8 +156,10 @@ __global__ void __launch_bounds__(256, 2) isvd_grid_kernel(IsvdBufs B) {
       for (long long i = tid; i < n; i += 256) {
         double qq[RMAX], pr[RMAX];
 #pragma unroll
+        for (int l = 0; l < RMAX; ++l) qq[l] = B.q[i + coff[l]];
+#pragma unroll
         for (int l = 0; l < RMAX; ++l) {
-          qq[l] = l < r ? B.q[i + (long long)l * n] : 0.0;
+          qq[l] *= mk[l];
           pr[l] = qq[l] * sp1[l];
         }
         const double e1 = B.b[i] - tree_sum<RMAX>(pr);
