@@ -55,8 +55,10 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs t) {
 #pragma unroll
     for (int q = 0; q < NT; ++q) {
       const int i = lane + 32 * q;
-      xv[q] = i < n ? xf[(long long)i * left] : 0.0;
+      xv[q] = xf[(long long)(i < n ? i : 0) * left];  // unconditional: loads issue together
     }
+#pragma unroll
+    for (int q = 0; q < NT; ++q) xv[q] *= (lane + 32 * q < n) ? 1.0 : 0.0;
   };
   bool have = false;
   if (t.m0 < t.m1 && gw < t.left[t.m0] * t.right[t.m0]) {
@@ -75,7 +77,8 @@ __global__ void __launch_bounds__(256) tail_kernel(TailArgs t) {
     for (int s2 = 0; s2 < PER; ++s2) {
       const int idx = threadIdx.x + 256 * s2;
       const int i = idx % NP, j = idx / NP;
-      tmp[s2] = (idx < TOT && i < n && j < R) ? u[i + (long long)j * n] : 0.0;
+      const bool ok = idx < TOT && i < n && j < R;
+      tmp[s2] = u[ok ? i + (long long)j * n : 0] * (ok ? 1.0 : 0.0);
     }
 #pragma unroll
     for (int s2 = 0; s2 < PER; ++s2) {
