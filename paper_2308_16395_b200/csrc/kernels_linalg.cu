@@ -1,3 +1,4 @@
+#include <cstdlib>
 // Dense linear algebra kernels of the B200 streaming ST-HOSVD engine:
 // Jacobi eigensolver, truncation rule, Gram (SYRK) kernels, MGS and the
 // tensor relayouts used by basis expansion and stream_init.
@@ -807,7 +808,11 @@ __global__ void __launch_bounds__(256) sym_eig_coop_kernel(const double* __restr
 // Large n: cooperative grid (one CTA per SM at most); small n: one CTA.
 bool launch_sym_eig_coop(const double* g, int n, double* evals, double* evecs, double* work,
                          double* part, int* sweeps_out, cudaStream_t st) {
-  if (n < 96) return false;
+  static const int min_n = [] {  // below: the single-CTA solver (TSG_COOP_EIG_MIN)
+    const char* e = std::getenv("TSG_COOP_EIG_MIN");
+    return e ? std::atoi(e) : 96;
+  }();
+  if (n < min_n) return false;
   int dev = 0, coop = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
