@@ -10,8 +10,12 @@ synthetic slice of the BASELINE configuration (default configs[1], "c2":
 
 Our arm: slices are synthesised on the device before the timed region and
 each step reads a distinct slice (never re-read), so no step hits L2 with
-its input. W untimed updates, then K timed updates bracketed by a barrier and
-synchronisation; time = CUDA events on the engine's stream, max over ranks.
+its input. W untimed updates (at least 12: the engine's graph keys), then K
+timed updates bracketed by a barrier and synchronisation; time = CUDA events
+on the engine's stream, max over ranks. The headline pass carries no
+per-phase event nodes; a second timed pass over the same slices with
+per-phase CUDA events gives the mode-0 kernel's live duration (roofline) and
+the phase breakdown (multi-GB slices: one pass with mode-0 events only).
 For N>1 (torchrun) the default is the sharded engine: one
 stream, each slice split along its last spatial mode over the GPUs, one NCCL
 allgather per slice, "scaling": "strong"; --mode replicas runs independent
