@@ -420,6 +420,7 @@ def run_sharded(args, world, rank, local):
         host = [torch.empty(slabs[0].numel(), dtype=torch.float64, pin_memory=True) for _ in range(nh)]
         for j, h in enumerate(host):
             h.copy_(slabs[j % nsl].cpu())
+        st.stream_update_slab(host[0], comm)  # untimed: host-slab staging allocation
         barrier(world)
         torch.cuda.synchronize()
         t0 = time.perf_counter()

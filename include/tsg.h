@@ -165,9 +165,10 @@ int tsg_error_sums(tsg_stream* h, const double* x, int64_t t0, int64_t count,
  *       tsg_shard_continue(h, &ex)
  *     }
  *
- * The exchange buffers are device memory owned by the handle; the collective
- * must be complete, or enqueued on tsg_cuda_stream(h), when
- * tsg_shard_continue is called. In steady state there is exactly one
+ * The exchange buffers are device memory owned by the handle. The request is
+ * returned once the local pass is ENQUEUED on tsg_cuda_stream(h): the
+ * collective must be enqueued on that stream (or follow a synchronisation),
+ * and be complete or enqueued there when tsg_shard_continue is called. In steady state there is exactly one
  * exchange per slice (the compressed local tensor plus partial norms);
  * growth of a basis k < s adds one more. Every reduction over ranks runs in
  * rank order on the gathered bytes, so all ranks end bitwise identical. */

@@ -1248,8 +1248,9 @@ struct tsg_stream {
                          cudaMemcpyDeviceToDevice, st), "slab copy");
     if (header > 0) launch_shard_pack_pairs(sp, sh_send, st);
   }
+  // The request is returned as soon as the local pass is enqueued: the
+  // caller's collective must run on tsg_cuda_stream(h) (or after a sync).
   void shard_request(tsg_exchange* ex) {
-    ck(cudaStreamSynchronize(st), "cudaStreamSynchronize");
     ck(cudaGetLastError(), "shard local pass");
     ex->pending = 1;
     ex->count = sh_count;
@@ -1258,9 +1259,15 @@ struct tsg_stream {
   }
   void shard_done(tsg_exchange* ex) {
     sh_phase = 0;
-    sync();
+    // the slice's record arrives through the mapped ring (no stream sync and
+    // no control-block copy on the way out)
     drain(true);
-    pull_ctrl();
+    if (have_last_ctrl && pending.empty()) {
+      *ctrl_h = last_ctrl;
+      ck(cudaGetLastError(), "kernel");
+    } else {
+      pull_ctrl();
+    }
     r_exact = ctrl_h->r;
     ex->pending = 0;
     ex->count = 0;
@@ -1272,7 +1279,7 @@ struct tsg_stream {
     if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
     if (shard_world == 0) fail(TSG_EINVAL, "tsg_shard_begin: call tsg_shard_setup first");
     if (sh_phase != 0) fail(TSG_EINVAL, "tsg_shard_begin: the previous slice's exchange is pending");
-    flush();
+    if (have_prev || !pending.empty()) flush();  // a preceding async tsg_update
     sh_t0 = std::chrono::steady_clock::now();
     const int s = d - 2;
     const long long le = prod(N, s) * shard_n[shard_rank];
@@ -1353,9 +1360,13 @@ struct tsg_stream {
       ydk[k] = R[k];
       cur = out;
     }
+    // the decision comes back through the mapped slot (a spin, no copy call)
+    da.host_slot = hslot_d;
+    da.seq_counter = seq_dev;
+    ++seq_expect[0];
     launch_decide(da, st);
-    pull_slot(0);
-    const SliceCtl sc = slots_h[0];
+    const SliceCtl sc = wait_slot(0);
+    slots_h[0] = sc;  // run_growth reads the delta of a local-mode growth from here
     if (sc.zero_slice) {
       zero_slice_path(0, sh_t0);
     } else if (sc.expand_mode < 0) {

@@ -166,6 +166,7 @@ class LoopbackGroup:
                 return
             if not all(pend) or len({int(e.count) for e in exs}) != 1:
                 raise RuntimeError(f"ranks diverged: pending {pend}, counts {[e.count for e in exs]}")
+            torch.cuda.synchronize()  # the local passes run on the engines' streams
             views = [st.exchange_tensors(e) for st, e in zip(self.states, exs)]
             cnt = int(exs[0].count)
             for _, recv in views:
