@@ -632,6 +632,9 @@ struct tsg_stream {
     launch_gemm_nn(A, rows, vec, cols, basis, rows, rows, (int)s.rank, (int)cols, st);
     launch_scale_cols_invsqrt(basis, rows, rows, (int)s.rank, ev, st);
     launch_mgs(basis, rows, rows, (int)s.rank, st);
+    // callers copy the basis out on another stream: complete it here
+    sync();
+    ck(cudaGetLastError(), "mode_subspace");
     s.basis = basis;
     s.evals = ev;
     return s;

@@ -318,6 +318,101 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const double* __restr
     }
 }
 
+// Same partial Gram on the FP64 tensor cores: mma.sync m8n8k4 f64, a 64x64
+// tile per CTA of four warps, warp (wr, wc) owns the 32x32 quarter
+// (4 x 4 accumulator tiles: 16 DMMA per 8 fragment loads). K chunks of DK
+// columns are staged in shared memory (pitch 72 doubles: the fragment reads
+// of one warp hit every bank pair twice, the minimum for 32 x 8 bytes) and the
+// next chunk is held in registers while the current one is consumed. Rows /
+// columns past the end are zero.
+constexpr int DK = 32;
+constexpr int DPITCH = GT + 8;
+constexpr int DTHREADS = 128;
+
+__device__ __forceinline__ void gram_dmma(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(DTHREADS) gram_partial_dmma_kernel(const double* __restrict__ a,
+                                                                     int rows, long long cols,
+                                                                     long long chunk,
+                                                                     double* __restrict__ partial) {
+  const int nt = (rows + GT - 1) / GT;
+  int t = blockIdx.x, ti = 0;
+  while (t >= nt - ti) {
+    t -= nt - ti;
+    ++ti;
+  }
+  const int tj = ti + t;
+  const long long c0 = (long long)blockIdx.y * chunk;
+  const long long c1 = min(cols, c0 + chunk);
+  __shared__ __align__(16) double As[DK][DPITCH];
+  __shared__ __align__(16) double Bs[DK][DPITCH];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  const int wr = warp & 1, wc = warp >> 1;
+  const int i0 = ti * GT, j0 = tj * GT;
+  // staging: thread -> row ii = tid % 64, columns kk = kb + 2 e (e < DK / 2)
+  constexpr int KS = DTHREADS / GT, NE = DK / KS;
+  const int ii = threadIdx.x % GT, kb = threadIdx.x / GT;
+  const bool iv = i0 + ii < rows, jv = j0 + ii < rows;
+  const int ic = iv ? i0 + ii : rows - 1, jc = jv ? j0 + ii : rows - 1;
+  double ra[NE], rb[NE];
+  auto fetch = [&](long long cc) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const long long c = cc + kb + KS * e;
+      const bool cv = c < c1;
+      const long long cl = cv ? c : c1 - 1;
+      const double va = __ldg(a + ic + cl * rows);
+      const double vb = __ldg(a + jc + cl * rows);
+      ra[e] = (cv && iv) ? va : 0.0;
+      rb[e] = (cv && jv) ? vb : 0.0;
+    }
+  };
+  double acc[4][4][2];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  if (c0 < c1) fetch(c0);
+  for (long long cc = c0; cc < c1; cc += DK) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      As[kb + KS * e][ii] = ra[e];
+      Bs[kb + KS * e][ii] = rb[e];
+    }
+    __syncthreads();
+    if (cc + DK < c1) fetch(cc + DK);
+#pragma unroll
+    for (int ks = 0; ks < DK / 4; ++ks) {
+      const int k = 4 * ks + tq;
+      double af[4], bf[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) af[x] = As[k][32 * wr + 8 * x + g];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) bf[y] = Bs[k][32 * wc + 8 * y + g];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) gram_dmma(acc[x][y][0], acc[x][y][1], af[x], bf[y]);
+    }
+    __syncthreads();
+  }
+  double* out = partial + (long long)blockIdx.y * rows * rows;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = i0 + 32 * wr + 8 * x + g, j = j0 + 32 * wc + 8 * y + 2 * tq + h;
+        if (i < rows && j < rows) out[i + (long long)j * rows] = acc[x][y][h];
+      }
+}
+
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int rows, int splits,
                                    double* __restrict__ g) {
   const long long total = (long long)rows * rows;
@@ -523,10 +618,19 @@ void launch_truncate(double* evals, int n, double delta, int zero_floor, long lo
 int gram_splits(int rows, long long cols) {
   const int nt = (rows + GT - 1) / GT;
   const int tiles = nt * (nt + 1) / 2;
-  long long s = (2LL * kNumSMs + tiles - 1) / tiles;
+  static const long long waves = [] {  // TSG_GRAM_WAVES: CTAs per SM targeted
+    const char* e = std::getenv("TSG_GRAM_WAVES");
+    return e ? std::atoll(e) : 8LL;
+  }();
+  long long s = (waves * kNumSMs + tiles - 1) / tiles;
   const long long max_by_cols = (cols + 4 * GK - 1) / (4 * GK);
   if (s > max_by_cols) s = max_by_cols;
-  if (s > 256) s = 256;
+  // narrow modes need many CTAs to keep enough bytes in flight; the partial
+  // buffer (splits x rows^2) stays <= 32 Mi doubles
+  long long cap = (1LL << 25) / ((long long)rows * rows);
+  if (cap < 256) cap = 256;
+  if (cap > 4096) cap = 4096;
+  if (s > cap) s = cap;
   if (s < 1) s = 1;
   return (int)s;
 }
@@ -538,7 +642,14 @@ void launch_gram(const double* a, int rows, long long cols, double* g, double* p
   const int splits = gram_splits(rows, cols);
   long long chunk = (cols + splits - 1) / splits;
   chunk = (chunk + GK - 1) / GK * GK;
-  gram_partial_kernel<<<dim3(tiles, splits), 256, 0, st>>>(a, rows, cols, chunk, partial);
+  static const bool ffma = [] {  // TSG_GRAM_FFMA=1: the CUDA-core SYRK (A/B)
+    const char* e = std::getenv("TSG_GRAM_FFMA");
+    return e && std::atoi(e) != 0;
+  }();
+  if (ffma)
+    gram_partial_kernel<<<dim3(tiles, splits), 256, 0, st>>>(a, rows, cols, chunk, partial);
+  else
+    gram_partial_dmma_kernel<<<dim3(tiles, splits), DTHREADS, 0, st>>>(a, rows, cols, chunk, partial);
   gram_reduce_kernel<<<grid_for((long long)rows * rows), 256, 0, st>>>(partial, rows, splits, g);
   g_launches += 2;
 }

@@ -379,3 +379,46 @@ def test_config4_wide_mode0_vs_oracle(oracle, graphs, monkeypatch):
     print("c4_wide", graphs, mc, sc)
     assert sc["factors_raw"] <= 1e-7, sc
     P.assert_parity(mc, sc, resid_tol=5e-8)
+
+
+@pytest.mark.parametrize("dims,mode", [
+    ((7, 3, 5), 0),          # rows below one MMA tile
+    ((63, 40, 3), 0),        # ragged last 8-row group
+    ((64, 33, 2), 0),        # exactly one 64-row tile, ragged K chunk
+    ((65, 9, 31), 0),        # one row past a tile
+    ((130, 70, 11), 0),      # three row tiles (off-diagonal tiles), split K
+    ((9, 200, 17), 1),       # an interior mode (unfolded first)
+    ((6, 5, 97), 2),         # the last mode
+])
+def test_mode_subspace_gram_vs_numpy(dims, mode):
+    """The Gram route of mode_subspace (the residual SYRK on the FP64 tensor
+    cores, then the Jacobi eigensolver) against float64 numpy: eigenvalues of
+    X_(k) X_(k)^T and the retained basis' subspace, ragged tile edges
+    included."""
+    g = np.random.default_rng(sum(dims) + mode)
+    t = g.standard_normal(dims)
+    a = np.moveaxis(t, mode, 0).reshape(dims[mode], -1)
+    w = np.linalg.eigvalsh(a @ a.T)[::-1]
+    basis, ev, disc = S.mode_subspace(t, mode, 0.3 * np.linalg.norm(t))
+    np.testing.assert_allclose(ev, np.maximum(w, 0), rtol=0, atol=1e-12 * w[0])
+    r = basis.shape[1]
+    assert r >= 1
+    # the retained columns span the top-r eigenspace (projector distance)
+    v = np.linalg.eigh(a @ a.T)[1][:, ::-1][:, :r]
+    if r < len(w) and w[r - 1] - w[r] > 1e-6 * w[0]:
+        pa, pb = basis @ basis.T, v @ v.T
+        assert np.abs(pa - pb).max() < 1e-9
+    assert disc == pytest.approx(w[r:].sum(), rel=1e-10, abs=1e-12 * w[0])
+
+
+@pytest.mark.parametrize("dims", [(16, 40, 300), (5, 7, 900), (32, 64, 50), (33, 20, 80)])
+def test_mode_subspace_gram_narrow_modes(dims):
+    """Narrow modes (rows <= 32: the Gram's K steps are split over the warps
+    and summed in a fixed order) and the first size past it, against numpy."""
+    g = np.random.default_rng(dims[0] * 7 + dims[2])
+    t = g.standard_normal(dims)
+    a = t.reshape(dims[0], -1)
+    w = np.linalg.eigvalsh(a @ a.T)[::-1]
+    basis, ev, disc = S.mode_subspace(t, 0, 0.2 * np.linalg.norm(t))
+    np.testing.assert_allclose(ev, np.maximum(w, 0), rtol=0, atol=1e-12 * w[0])
+    assert disc == pytest.approx(w[basis.shape[1]:].sum(), rel=1e-10, abs=1e-12 * w[0])
