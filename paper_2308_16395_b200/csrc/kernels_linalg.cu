@@ -413,6 +413,96 @@ __global__ void __launch_bounds__(DTHREADS) gram_partial_dmma_kernel(const doubl
       }
 }
 
+// Narrow modes (rows <= 8 TX <= 32): one diagonal tile of 8 TX rows holds the
+// whole Gram, so each of the four warps computes all TX x TX MMA tiles over
+// its share of the K steps (warp w: steps w, w + 4, ...; no per-MMA guards,
+// rows past the end are zero in shared memory) and the four partial tiles
+// are summed in warp order at the end.
+constexpr int NK = 64;       // columns per staged chunk
+constexpr int NPITCH = 40;   // 40 mod 16 = 8: conflict-free fragment reads
+template <int TX>
+__global__ void __launch_bounds__(128) gram_partial_narrow_kernel(const double* __restrict__ a,
+                                                                  int rows, long long cols,
+                                                                  long long chunk,
+                                                                  double* __restrict__ partial) {
+  constexpr int RT = 8 * TX;
+  const long long c0 = (long long)blockIdx.y * chunk;
+  const long long c1 = min(cols, c0 + chunk);
+  constexpr int SMD = (NK * NPITCH > 3 * 32 * TX * TX * 2) ? NK * NPITCH : 3 * 32 * TX * TX * 2;
+  __shared__ __align__(16) double sm[SMD];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  // staging: thread -> row ii = tid % RT, columns kb + (128 / RT) e
+  constexpr int KS = 128 / RT, NE = NK / KS;
+  const int ii = threadIdx.x % RT, kb = threadIdx.x / RT;
+  const bool iv = ii < rows;
+  const int ic = iv ? ii : rows - 1;
+  double ra[NE];
+  auto fetch = [&](long long cc) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const long long c = cc + kb + KS * e;
+      const bool cv = c < c1;
+      const long long cl = cv ? c : c1 - 1;
+      const double v = __ldg(a + ic + cl * rows);
+      ra[e] = (cv && iv) ? v : 0.0;
+    }
+  };
+  double acc[TX][TX][2];
+#pragma unroll
+  for (int x = 0; x < TX; ++x)
+#pragma unroll
+    for (int y = 0; y < TX; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
+  if (c0 < c1) fetch(c0);
+  for (long long cc = c0; cc < c1; cc += NK) {
+#pragma unroll
+    for (int e = 0; e < NE; ++e) sm[(kb + KS * e) * NPITCH + ii] = ra[e];
+    __syncthreads();
+    if (cc + NK < c1) fetch(cc + NK);
+#pragma unroll
+    for (int s4 = 0; s4 < NK / 16; ++s4) {
+      const int k = 4 * (4 * s4 + warp) + tq;
+      double f[TX];
+#pragma unroll
+      for (int x = 0; x < TX; ++x) f[x] = sm[k * NPITCH + 8 * x + g];
+#pragma unroll
+      for (int x = 0; x < TX; ++x)
+#pragma unroll
+        for (int y = 0; y < TX; ++y) gram_dmma(acc[x][y][0], acc[x][y][1], f[x], f[y]);
+    }
+    __syncthreads();
+  }
+  constexpr int PER = TX * TX * 2;
+  if (warp > 0) {
+#pragma unroll
+    for (int x = 0; x < TX; ++x)
+#pragma unroll
+      for (int y = 0; y < TX; ++y)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) sm[((warp - 1) * PER + (x * TX + y) * 2 + h) * 32 + lane] = acc[x][y][h];
+  }
+  __syncthreads();
+  if (warp != 0) return;
+#pragma unroll
+  for (int w = 0; w < 3; ++w)
+#pragma unroll
+    for (int x = 0; x < TX; ++x)
+#pragma unroll
+      for (int y = 0; y < TX; ++y)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) acc[x][y][h] += sm[(w * PER + (x * TX + y) * 2 + h) * 32 + lane];
+  double* out = partial + (long long)blockIdx.y * rows * rows;
+#pragma unroll
+  for (int x = 0; x < TX; ++x)
+#pragma unroll
+    for (int y = 0; y < TX; ++y)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = 8 * x + g, j = 8 * y + 2 * tq + h;
+        if (i < rows && j < rows) out[i + (long long)j * rows] = acc[x][y][h];
+      }
+}
+
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int rows, int splits,
                                    double* __restrict__ g) {
   const long long total = (long long)rows * rows;
@@ -427,6 +517,28 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int rows,
     double s = 0.0;
     for (int sp = 0; sp < splits; ++sp) s += partial[(long long)sp * total + i + (long long)j * rows];
     g[idx] = s;
+  }
+}
+
+// Small Grams with many K splits: one warp per (upper) element, lanes take
+// the splits strided by 32, then a fixed butterfly (deterministic order).
+__global__ void gram_reduce_warp_kernel(const double* __restrict__ partial, int rows, int splits,
+                                        double* __restrict__ g) {
+  const long long total = (long long)rows * rows;
+  const int lane = threadIdx.x & 31;
+  for (long long idx = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5; idx < total;
+       idx += ((long long)gridDim.x * blockDim.x) >> 5) {
+    int i = (int)(idx % rows), j = (int)(idx / rows);
+    if (i > j) {
+      const int t = i;
+      i = j;
+      j = t;
+    }
+    double s = 0.0;
+    for (int sp = lane; sp < splits; sp += 32) s += partial[(long long)sp * total + i + (long long)j * rows];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) g[idx] = s;
   }
 }
 
@@ -648,9 +760,17 @@ void launch_gram(const double* a, int rows, long long cols, double* g, double* p
   }();
   if (ffma)
     gram_partial_kernel<<<dim3(tiles, splits), 256, 0, st>>>(a, rows, cols, chunk, partial);
+  else if (rows <= 16)
+    gram_partial_narrow_kernel<2><<<dim3(1, splits), 128, 0, st>>>(a, rows, cols, chunk, partial);
+  else if (rows <= 32)
+    gram_partial_narrow_kernel<4><<<dim3(1, splits), 128, 0, st>>>(a, rows, cols, chunk, partial);
   else
     gram_partial_dmma_kernel<<<dim3(tiles, splits), DTHREADS, 0, st>>>(a, rows, cols, chunk, partial);
-  gram_reduce_kernel<<<grid_for((long long)rows * rows), 256, 0, st>>>(partial, rows, splits, g);
+  if ((long long)rows * rows <= 64LL * 64 && splits >= 64)
+    gram_reduce_warp_kernel<<<(int)std::min<long long>(((long long)rows * rows + 7) / 8, 8LL * kNumSMs),
+                              256, 0, st>>>(partial, rows, splits, g);
+  else
+    gram_reduce_kernel<<<grid_for((long long)rows * rows), 256, 0, st>>>(partial, rows, splits, g);
   g_launches += 2;
 }
 
