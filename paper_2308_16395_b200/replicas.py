@@ -1,13 +1,13 @@
 """Multi-GPU plumbing for the streamed update: independent replicas.
 
-SURVEY §8(e): a streaming ST-HOSVD state is a single sequential chain (slice
-t+1's projection needs the bases slice t may have grown), so one stream does
-not shard without a per-slice exchange. What scales is independent streams:
-each rank (one process per GPU, launched by torchrun) owns its own stream —
-its own seeded slice sequence — and no data-path collective exists. The only
-collectives are the benchmark's barrier and the max/sum reductions of its
-timing, which this module wraps so the same code runs over NCCL on GPUs and
-over gloo on CPU (tests/test_replicas.py, world_size 2).
+This is the `--mode replicas` alternative to the sharded single stream
+(`sharded.py`): each rank (one process per GPU, launched by
+torchrun) owns its own stream — its own seeded slice sequence — and no
+data-path collective exists. The only collectives are the benchmark's barrier
+and the max/sum reductions of its timing, which this module wraps so the same
+code runs over NCCL on GPUs and over gloo on CPU (tests/test_replicas.py,
+world_size 2). The default multi-GPU mode is the sharded one, where a single
+stream's slices are split along a spatial mode with one exchange per slice.
 """
 from __future__ import annotations
 
