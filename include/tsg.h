@@ -39,7 +39,10 @@
  * StreamingState::streaming_factor() returns it.
  *
  * Memory: TSG_MEM_HOST slices are copied to device staging on a copy
- * stream; TSG_MEM_DEVICE pointers must be device-resident fp64 buffers. In
+ * stream; TSG_MEM_DEVICE pointers must be device-resident fp64 buffers. The
+ * handle's stream (tsg_cuda_stream) is a blocking stream: device reads of a
+ * slice are ordered after work queued earlier on the legacy default stream;
+ * a producer on another non-blocking stream must synchronise first. In
  * the default synchronous mode a slice may be reused as soon as tsg_update
  * returns. With TSG_ASYNC, a slice (host or device) must stay unchanged
  * until the following tsg_update (or tsg_synchronize) returns.

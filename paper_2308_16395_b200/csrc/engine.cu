@@ -1960,7 +1960,10 @@ int tsg_create(const tsg_config* cfg, tsg_stream** out) {
     ck(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
     if (h->device < 0 || h->device >= n) fail(TSG_EDEVICE, "no such CUDA device");
     ck(cudaSetDevice(h->device), "cudaSetDevice");
-    ck(cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking), "cudaStreamCreate");
+    // a BLOCKING stream: the engine's reads of a caller's device slice are
+    // ordered after work the caller queued on the legacy default stream (where
+    // torch, cudaMemcpy and most producers write it) with no per-call API cost
+    ck(cudaStreamCreate(&h->st), "cudaStreamCreate");
     h->launches_at_create = g_launches;
   });
   if (st) {
