@@ -2182,7 +2182,7 @@ int tsg_debug_project(const double* x, int64_t left, int64_t n, int64_t right, c
     a.debug_skip = flags & 7;
     // TMA mode-0 kernel profiling switches: 64 stream only; 128 / 256 / 512 skip
     // the cross-warp reduction / phase 2 / phase 1 (results then meaningless)
-    a.karg1 = (flags & 64) ? 7 : (((flags >> 7) & 7) << 3);
+    a.karg1 = (flags & 64) ? 7 : ((((flags >> 7) & 7) << 3) | (((flags >> 10) & 1) << 6));
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);

@@ -83,6 +83,9 @@ struct ProjArgs {
 // multiple of 8, row pitch 8*ceil(R/8)+4, zero fill. Returns its size in
 // doubles for (N, R); writes it when `out` is non-null.
 long long upad_size(long long N, int R);
+// Offset (doubles) of the column-owning kernel's U images inside the pad_u
+// buffer (N a multiple of 8): [image 1 (N x (8RT+2)) | image 2 (N x (8RT+4))].
+long long upad_cols_offset(long long N, int R);
 void launch_pad_u(const double* u, long long N, int R, double* out, cudaStream_t st);
 // Returns the grid size (number of partial pairs written).
 int launch_project(const ProjArgs& a, cudaStream_t st);

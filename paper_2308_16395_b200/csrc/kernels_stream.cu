@@ -7,6 +7,8 @@
 
 #include "kernels.cuh"
 #include "proj_dmma.cuh"
+#include "proj0_fma.cuh"
+#include "proj0_cols.cuh"
 #include "decide.cuh"
 
 namespace tsg {
@@ -160,12 +162,41 @@ __global__ void pad_u_kernel(const double* __restrict__ u, long long N, int R, i
   }
 }
 
+// The column-owning mode-0 kernel's two U images (proj0_cols.cuh), stored
+// right after the row-split image: image 1 (pitch 8RT+2) holds rank
+// 8nt+4i+t in column 8nt+2t+i, image 2 (pitch 8RT+4) natural rank order.
+__global__ void cols_u_kernel(const double* __restrict__ u, long long N, int R, int RT,
+                              double* __restrict__ out) {
+  const int p1 = 8 * RT + 2, p2 = 8 * RT + 4;
+  const long long total = N * (p1 + p2);
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    int rk;
+    long long row;
+    if (idx < N * p1) {
+      row = idx / p1;
+      const int col = (int)(idx % p1);
+      rk = col < 8 * RT ? (col & ~7) + 4 * (col & 1) + ((col & 7) >> 1) : R;
+    } else {
+      const long long j2 = idx - N * p1;
+      row = j2 / p2;
+      rk = (int)(j2 % p2);
+      if (rk >= 8 * RT) rk = R;
+    }
+    out[idx] = rk < R ? u[row + rk * N] : 0.0;
+  }
+}
+
 }  // namespace
 
 long long upad_size(long long N, int R) {
   const long long rows8 = (N + 7) / 8 * 8;
   const int rpad = 8 * ((R + 7) / 8) + 4;
-  return rows8 * rpad;
+  return rows8 * rpad + rows8 * (16 * ((R + 7) / 8) + 6);
+}
+
+long long upad_cols_offset(long long N, int R) {
+  return (N + 7) / 8 * 8 * (8 * ((R + 7) / 8) + 4);
 }
 
 void launch_pad_u(const double* u, long long N, int R, double* out, cudaStream_t st) {
@@ -173,6 +204,12 @@ void launch_pad_u(const double* u, long long N, int R, double* out, cudaStream_t
   const int rpad = 8 * ((R + 7) / 8) + 4;
   pad_u_kernel<<<(int)((rows8 * rpad + 255) / 256), 256, 0, st>>>(u, N, R, rpad, rows8, out);
   ++g_launches;
+  if (N % 8 == 0) {
+    const int RT = (R + 7) / 8;
+    cols_u_kernel<<<(int)((N * (16 * RT + 6) + 255) / 256), 256, 0, st>>>(u, N, R, RT,
+                                                                           out + rows8 * rpad);
+    ++g_launches;
+  }
 }
 
 namespace {
@@ -190,7 +227,9 @@ int launch_project(const ProjArgs& a, cudaStream_t st) {
   static const bool force_generic = std::getenv("TSG_GENERIC_PROJ") != nullptr;
   static const bool debug = std::getenv("TSG_DEBUG_SYNC") != nullptr;
   if (!force_generic) {
-    const int grid = dmma_proj::launch(a, a.stream_in, st);
+    int grid = a.debug_skip == 0 ? cols0::launch(a, st) : -1;
+    if (grid <= 0 && a.debug_skip == 0) grid = fma0::launch(a, st);
+    if (grid <= 0) grid = dmma_proj::launch(a, a.stream_in, st);
     if (debug) {
       cudaError_t e = cudaStreamSynchronize(st);
       if (e == cudaSuccess) e = cudaGetLastError();
