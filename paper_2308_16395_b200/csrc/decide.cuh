@@ -47,7 +47,27 @@ __device__ __forceinline__ void decide_finish(const DecideArgs& a, double xsq, c
     h->zero_slice = zero;
     const unsigned long long q = *a.seq_counter + 1;
     *a.seq_counter = q;
+    unsigned long long D = 0;
+    if (a.ring_dev) {
+      // insertion records completed so far (gpu-scope acquire), copied to the
+      // host ring before the one system fence below
+      D = *reinterpret_cast<const volatile unsigned long long*>(&a.ring_dev->done);
+      __threadfence();
+      unsigned long long P = *a.ring_pub;
+      if (D > P + kRecRing - 1) P = D - (kRecRing - 1);
+      for (unsigned long long k = P; k < D; ++k) {
+        const int pos = (int)(k % kRecRing);
+        const unsigned long long* sm = reinterpret_cast<const unsigned long long*>(&a.ring_dev->rec[pos]);
+        unsigned long long* dm = reinterpret_cast<unsigned long long*>(&a.ring_host->rec[pos]);
+        for (int w = 0; w < (int)(sizeof(Metrics) / 8); ++w) dm[w] = __ldcg(sm + w);
+        const unsigned long long* sc = reinterpret_cast<const unsigned long long*>(&a.ring_dev->ctrl[pos]);
+        unsigned long long* dc = reinterpret_cast<unsigned long long*>(&a.ring_host->ctrl[pos]);
+        for (int w = 0; w < (int)(sizeof(Ctrl) / 8); ++w) dc[w] = __ldcg(sc + w);
+      }
+      *a.ring_pub = D > P ? D : P;
+    }
     __threadfence_system();
+    if (a.ring_dev) *reinterpret_cast<volatile unsigned long long*>(&a.ring_host->done) = D;
     *reinterpret_cast<volatile unsigned long long*>(&h->seq) = q;
   }
 }

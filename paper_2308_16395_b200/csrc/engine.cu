@@ -125,8 +125,11 @@ struct tsg_stream {
   SliceCtl* hslot_d = nullptr;
   unsigned long long* seq_dev = nullptr;  // device [kNP] decision counters
   unsigned long long seq_expect[kNP] = {};
-  RecRing* ring_h = nullptr;              // mapped
-  RecRing* ring_d = nullptr;
+  RecRing* ring_h = nullptr;              // mapped (published by the tail kernels)
+  RecRing* ring_d = nullptr;              // device alias of ring_h
+  RecRing* ring_dev = nullptr;            // device ring the insertion kernels write
+  unsigned long long* ring_pub = nullptr; // device: records copied to ring_h
+  RecRing ring_shadow{};                  // host copy of ring_dev at a forced drain
   unsigned long long rec_read = 0;        // records consumed by the host
   struct Pending {
     int mask;
@@ -506,16 +509,28 @@ struct tsg_stream {
 
   // ---------------------------------------------------- metrics drain
   // Retire published insertions in order (all issued ones when `force`).
+  // Records reach the host two ways: published into the mapped ring by the
+  // tail kernels of later slices (non-forced drains read that), or copied
+  // from the device ring after a synchronisation (forced drains).
   void drain(bool force = true) {
     if (pending.empty()) return;
     const unsigned long long target = rec_read + pending.size();
-    if (force) spin([&] { return rec_done() >= target; }, "insertion record");
-    const unsigned long long done = rec_done();
-    std::atomic_thread_fence(std::memory_order_acquire);
+    const RecRing* src = ring_h;
+    unsigned long long done;
+    if (force) {
+      sync();
+      ck(cudaMemcpy(&ring_shadow, ring_dev, sizeof(RecRing), cudaMemcpyDeviceToHost), "record copy");
+      src = &ring_shadow;
+      done = ring_shadow.done;
+      if (done < target) fail(TSG_EDEVICE, "insertion record: device result was never published");
+    } else {
+      done = rec_done();
+      std::atomic_thread_fence(std::memory_order_acquire);
+    }
     while (rec_read < done && !pending.empty()) {
       const int pos = (int)(rec_read % kRecRing);
-      const Metrics m = ring_h->rec[pos];
-      const Ctrl cs = ring_h->ctrl[pos];
+      const Metrics m = src->rec[pos];
+      const Ctrl cs = src->ctrl[pos];
       const Pending p = pending.front();
       tsg_slice_metrics o;
       std::memset(&o, 0, sizeof o);
@@ -829,7 +844,7 @@ struct tsg_stream {
     B.partial = ipart;
     B.hand = isvd_hand;
     B.gsync = isvd_gsync;
-    B.ring = ring_d;
+    B.ring = ring_dev;
     B.n = n;
     B.cap_rows = cap_rows;
     B.capr = capr;
@@ -915,6 +930,9 @@ struct tsg_stream {
       da.slot = slots + par;
       da.host_slot = hslot_d + par;
       da.seq_counter = seq_dev + par;
+      da.ring_dev = ring_dev;
+      da.ring_host = ring_d;
+      da.ring_pub = ring_pub;
       da.nmodes = d - 1;
       da.tau = tau;
       da.order = d;
@@ -1089,7 +1107,7 @@ struct tsg_stream {
       reserve_record();
       long long sp[kMaxD] = {0};
       for (int k = 0; k + 1 < d; ++k) sp[k] = R[k];
-      launch_zero_slice(ctrl, slots + par, left, capr, ring_d, d, sp, st);
+      launch_zero_slice(ctrl, slots + par, left, capr, ring_dev, d, sp, st);
       ck(cudaEventRecord(ev_isvd[par], st), "cudaEventRecord");
       ev_isvd_valid[par] = true;
       ++n_d;
@@ -1630,6 +1648,10 @@ struct tsg_stream {
     hslot_d = static_cast<SliceCtl*>(dp);
     ck(cudaHostGetDevicePointer(&dp, ring_h, 0), "cudaHostGetDevicePointer");
     ring_d = static_cast<RecRing*>(dp);
+    ring_dev = reinterpret_cast<RecRing*>(dalloc((sizeof(RecRing) + 7) / 8));
+    ck(cudaMemsetAsync(ring_dev, 0, sizeof(RecRing), st), "memset");
+    ring_pub = reinterpret_cast<unsigned long long*>(dalloc(1));
+    ck(cudaMemsetAsync(ring_pub, 0, 8, st), "memset");
     seq_dev = reinterpret_cast<unsigned long long*>(dalloc(kNP));
     ck(cudaMemsetAsync(seq_dev, 0, kNP * sizeof(unsigned long long), st), "memset");
     // grid-insertion handoff + handshake words (zeroed before any insertion)

@@ -18,6 +18,7 @@
 // block barriers.
 #include <cstdio>
 #include <cstdlib>
+#include <cooperative_groups.h>
 
 #include "kernels.cuh"
 namespace tsg {
@@ -472,15 +473,16 @@ __device__ void pgram_block(const double* __restrict__ left, long long n_d, int 
   }
 }
 
-// Append a record to the host-mapped ring (metrics + control snapshot) and
-// publish it: fields, system fence, then the count.
+// Append a record to the device ring (metrics + control snapshot): fields,
+// gpu-scope fence, then the count. The host sees it once a tail kernel
+// (decide_finish) has copied it to the mapped ring, or by a copy at drain.
 __device__ void publish(Ctrl* c, const Metrics& m, RecRing* ring) {
   const unsigned long long k = c->records;
   const int pos = (int)(k % kRecRing);
   ring->rec[pos] = m;
   c->records = k + 1;
   ring->ctrl[pos] = *c;
-  __threadfence_system();
+  __threadfence();
   *reinterpret_cast<volatile unsigned long long*>(&ring->done) = k + 1;
 }
 
@@ -1060,6 +1062,8 @@ void ensure_smem(K kernel, size_t bytes) {
 
 #include "isvd_small.cuh"
 #include "isvd_grid.cuh"
+#include "isvd_cta.cuh"
+#include "isvd_clu.cuh"
 
 namespace {
 template <int RMAX, int RPT, bool QREG = true>
@@ -1079,12 +1083,78 @@ void launch_grid(const IsvdBufs& B, cudaStream_t st) {
   ensure_smem(isvd_grid_kernel<RMAX>, smem);
   isvd_grid_kernel<RMAX><<<G, 256, smem, st>>>(B);
 }
+template <int RMAX, int RPT>
+void launch_cta(const IsvdBufs& B, cudaStream_t st) {
+  const size_t smem = sizeof(double) * (size_t)cta::smem_doubles(B.n, B.r_hint);
+  ensure_smem(cta::isvd_cta_kernel<RMAX, RPT>, smem);
+  cta::isvd_cta_kernel<RMAX, RPT><<<1, cta::kThreads, smem, st>>>(B);
+}
+template <int RMAX>
+void launch_clu(const IsvdBufs& B, cudaStream_t st) {
+  // rows per CTA: even (16-byte aligned bulk copies), at most 128 (one per thread)
+  int G = (int)((B.n + clu::kT - 1) / clu::kT);
+  if (G > clu::kMaxG) G = clu::kMaxG;
+  if (G < 1) G = 1;
+  int R0 = (int)((B.n + G - 1) / G);
+  R0 = (R0 + 1) & ~1;
+  G = (int)((B.n + R0 - 1) / R0);
+  const size_t smem = sizeof(double) * (size_t)clu::smem_doubles(R0, B.r_hint);
+  ensure_smem(clu::isvd_clu_kernel<RMAX, 1>, smem);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G, 1, 1);
+  cfg.blockDim = dim3(clu::kT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = G;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, clu::isvd_clu_kernel<RMAX, 1>, B, R0);
+}
+void launch_clu_r(const IsvdBufs& B, cudaStream_t st) {
+  const int rh = B.r_hint;
+  if (rh <= 8) launch_clu<8>(B, st);
+  else if (rh <= 12) launch_clu<12>(B, st);
+  else if (rh <= 14) launch_clu<14>(B, st);
+  else if (rh <= 16) launch_clu<16>(B, st);
+  else if (rh <= 20) launch_clu<20>(B, st);
+  else launch_clu<24>(B, st);
+}
+void launch_cta_r(const IsvdBufs& B, cudaStream_t st) {
+  const int rh = B.r_hint;
+  if (rh <= 8) launch_cta<8, 4>(B, st);
+  else if (rh <= 12) launch_cta<12, 4>(B, st);
+  else if (rh <= 14) launch_cta<14, 4>(B, st);
+  else if (rh <= 16) launch_cta<16, 4>(B, st);
+  else if (rh <= 20) launch_cta<20, 4>(B, st);
+  else launch_cta<24, 4>(B, st);
+}
 // n <= 512 * RPT, r_hint <= RMAX; false when not applicable
 bool try_small(const IsvdBufs& B, cudaStream_t st) {
   static const bool off = std::getenv("TSG_OLD_ISVD") != nullptr;
   static const bool small_only = std::getenv("TSG_ISVD_SMALL") != nullptr;
+  static const int use_cta = [] {
+    const char* e = std::getenv("TSG_ISVD_CTA");
+    return e ? std::atoi(e) : 1;
+  }();
   if (off || B.r_hint < 1 || B.r_hint > 31) return false;
   const int rh = B.r_hint;
+  // single CTA, branch-free inner solve (isvd_cta.cuh)
+  // cluster of CTAs (isvd_clu.cuh): rows split, DSMEM reductions
+  if (use_cta == 1 && !small_only && B.n <= clu::kMaxG * clu::kT && B.n >= 64 && rh <= 24 &&
+      (B.n % 2) == 0) {
+    launch_clu_r(B, st);
+    return true;
+  }
+  // (Q columns and b bulk-copied to shared memory: even n, and they must fit)
+  if (use_cta && !small_only && B.n <= 4 * cta::kThreads && rh <= 24 && (B.n % 2) == 0 &&
+      sizeof(double) * cta::smem_doubles(B.n, rh) <= 227 * 1024) {
+    launch_cta_r(B, st);
+    return true;
+  }
   if (!small_only && B.hand && B.gsync && B.n <= kGridMaxRows) {
     if (rh <= 4) launch_grid<4>(B, st);
     else if (rh <= 8) launch_grid<8>(B, st);

@@ -522,7 +522,8 @@ __global__ void __launch_bounds__(512, 1) isvd_small_kernel(IsvdBufs B) {
       unsigned long long* dstc = reinterpret_cast<unsigned long long*>(&B.ring->ctrl[pos]);
       for (int w = lane; w < (int)(sizeof(Ctrl) / 8); w += 32) dstc[w] = srcc[w];
     }
-    __threadfence_system();
+    // device ring (gpu scope): the tail kernel publishes it to the host
+    __threadfence();
     __syncwarp();
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&B.ring->done) = kr + 1;
   }

@@ -106,6 +106,11 @@ struct DecideArgs {
   double tau;
   int order;
   int keep_delta = 0;        // use slot->delta as given (process_nonstreaming_mode)
+  // insertion records: copied from the device ring to the mapped host ring
+  // under the decision's system fence (keeps that fence off the insertion chain)
+  const RecRing* ring_dev = nullptr;
+  RecRing* ring_host = nullptr;
+  unsigned long long* ring_pub = nullptr;  // device: records already copied
 };
 void launch_decide(const DecideArgs& a, cudaStream_t st);
 
