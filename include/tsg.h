@@ -63,7 +63,8 @@ enum tsg_status {
   TSG_EINVAL = 1,   /* std::invalid_argument */
   TSG_EDRIFT = 2,   /* coupling drift: std::runtime_error */
   TSG_EOTHER = 3,
-  TSG_EDEVICE = 4   /* CUDA error */
+  TSG_EDEVICE = 4,  /* CUDA error */
+  TSG_EIO = 5       /* checkpoint file error: tucker::IoError (io.hpp:24-33) */
 };
 
 enum tsg_mem_kind { TSG_MEM_HOST = 0, TSG_MEM_DEVICE = 1 };
@@ -86,7 +87,7 @@ typedef struct {
   int32_t flags;             /* tsg_flags */
   int64_t rank_capacity;     /* initial streaming-rank capacity (0 = auto) */
   int64_t row_capacity;      /* initial n_d capacity (0 = auto) */
-  int64_t reorthogonalize_every; /* ISVDOptions (isvd.hpp:62-67); must be 0 */
+  int64_t reorthogonalize_every; /* ISVDOptions (isvd.hpp:62-67): MGS of both factors every K insertions, 0 = off */
 } tsg_config;
 
 /* Same layout as oracle/oracle_abi.h orc_dims. */
@@ -133,6 +134,15 @@ int tsg_import_state(tsg_stream* h, const tsg_dims* dims, const double* core,
                      const double* factors, const double* sigma,
                      const double* left, const double* right);
 double tsg_estimate_relative_error(tsg_stream* h);
+
+/* TUCKCKPT v1 checkpoint of the streaming state, byte-compatible with the
+ * reference's save_checkpoint / load_checkpoint + from_checkpoint
+ * (io.cpp:268-423, io.hpp): written atomically (path.tmp, then rename).
+ * Load validates the header like load_checkpoint (TSG_EIO on a bad magic,
+ * version, truncation or shape; TSG_EINVAL for a batch model) and assembles
+ * the state into h (TSG_EDRIFT if the core is not v x diag(s)). */
+int tsg_save_checkpoint(tsg_stream* h, const char* path);
+int tsg_load_checkpoint(tsg_stream* h, const char* path);
 
 int64_t tsg_metrics_count(tsg_stream* h);
 int tsg_metrics_at(tsg_stream* h, int64_t i, tsg_slice_metrics* out);

@@ -70,6 +70,8 @@ int ORC(metrics_at)(const orc_state* s, int64_t i, orc_metrics* out);
 int ORC(assemble)(const orc_dims* dims, const double* core,
                   const double* factors, const double* sigma,
                   const double* left, const double* right, orc_state** out);
+/* ISVDOptions::reorthogonalize_every of the state's ISVD (isvd.hpp:62-67). */
+int ORC(set_reorthogonalize_every)(orc_state* s, int64_t k);
 void ORC(destroy)(orc_state* s);
 const char* ORC(last_error)(void);
 

@@ -128,6 +128,7 @@ class Checker:
         self._ma = f("metrics_at"); self._ma.argtypes = [C.c_void_p, C.c_int64, C.POINTER(OrcMetrics)]
         self._as = f("assemble"); self._as.argtypes = [C.POINTER(OrcDims), _dp, _dp, _dp, _dp, _dp, C.POINTER(C.c_void_p)]
         self._de = f("destroy"); self._de.argtypes = [C.c_void_p]
+        self._sro = f("set_reorthogonalize_every"); self._sro.argtypes = [C.c_void_p, C.c_int64]
         self._le = f("last_error"); self._le.restype = C.c_char_p
         self._eig = f("sym_eig_desc"); self._eig.argtypes = [C.c_int64, _dp, _dp, _dp]
         self._tr = f("truncation_rank"); self._tr.argtypes = [C.c_int64, _dp, C.c_double]; self._tr.restype = C.c_int64
@@ -205,6 +206,14 @@ class Checker:
         self._check(self._ttm(_p(x), len(dims), d.ctypes.data_as(_i64p), mode, _p(af), a.shape[0], a.shape[1], int(transpose_a), _p(out)))
         return _unflat(out, od)
 
+    def load_checkpoint(self, path: str) -> "Handle":
+        """from_checkpoint(load_checkpoint(path)) (reference library only)."""
+        f = self.lib.tkr_load_checkpoint
+        f.argtypes = [C.c_char_p, C.POINTER(C.c_void_p)]
+        h = C.c_void_p()
+        self._check(f(path.encode(), C.byref(h)))
+        return Handle(self, h)
+
     def sum_of_squares(self, x: np.ndarray) -> float:
         x = np.ascontiguousarray(x, dtype=np.float64).ravel()
         return self._ss(_p(x), x.size)
@@ -228,6 +237,16 @@ class Handle:
     def stream_update(self, y: np.ndarray):
         y, _ = _flat(y)
         self.c._check(self.c._upd(self.h, _p(y)))
+
+    def save_checkpoint(self, path: str):
+        """save_checkpoint(path, state) (reference library only)."""
+        f = self.c.lib.tkr_save_checkpoint
+        f.argtypes = [C.c_void_p, C.c_char_p]
+        self.c._check(f(self.h, path.encode()))
+
+    def set_reorthogonalize_every(self, k: int):
+        """ISVDOptions::reorthogonalize_every of this state (isvd.hpp:62-67)."""
+        self.c._check(self.c._sro(self.h, int(k)))
 
     def update_flat(self, y: np.ndarray):
         y = np.ascontiguousarray(y, dtype=np.float64)

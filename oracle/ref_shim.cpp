@@ -17,6 +17,7 @@
 #include "tucker/sthosvd.hpp"
 #include "tucker/streaming.hpp"
 #include "tucker/tensor.hpp"
+#include "tucker/io.hpp"
 
 #define ORC(name) tkr_##name
 #include "oracle_abi.h"
@@ -200,6 +201,25 @@ int tkr_assemble(const orc_dims* dm, const double* core, const double* factors,
                                                              dm->nonstream_discarded_sq),
                             {}};
     *out = s;
+  });
+}
+
+int tkr_set_reorthogonalize_every(orc_state* s, int64_t k) {
+  return guarded([&] {
+    if (k < 0) throw std::invalid_argument("reorthogonalize_every must be nonnegative");
+    s->st.isvd.options.reorthogonalize_every = static_cast<std::size_t>(k);
+  });
+}
+
+// TUCKCKPT v1 (io.cpp:268-423) through the reference's own writer / reader.
+int tkr_save_checkpoint(const orc_state* s, const char* path) {
+  return guarded([&] { tucker::save_checkpoint(path, s->st); });
+}
+int tkr_load_checkpoint(const char* path, orc_state** out) {
+  *out = nullptr;
+  return guarded([&] {
+    auto* o = new orc_state{tucker::from_checkpoint(tucker::load_checkpoint(path)), {}};
+    *out = o;
   });
 }
 

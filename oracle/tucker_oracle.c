@@ -664,11 +664,37 @@ typedef struct {
   mat right; /* n x r */
   double squared_error;
   size_t insertions;
+  size_t reorthogonalize_every; /* ISVDOptions (isvd.hpp:62-67) */
 } isvd_t;
+
+/* GrowableRowMatrix::reorthogonalize (isvd.cpp:102-124): MGS over columns. */
+static void gm_reorthogonalize(growmat* g) {
+  for (size_t j = 0; j < g->cols; ++j) {
+    for (size_t i = 0; i < j; ++i) {
+      double dot = 0.0;
+      for (size_t r = 0; r < g->rows; ++r) {
+        const double* row = gm_row(g, r);
+        dot += row[i] * row[j];
+      }
+      for (size_t r = 0; r < g->rows; ++r) {
+        double* row = gm_row(g, r);
+        row[j] -= dot * row[i];
+      }
+    }
+    double sq = 0.0;
+    for (size_t r = 0; r < g->rows; ++r) {
+      const double v = gm_row(g, r)[j];
+      sq += v * v;
+    }
+    const double norm = sqrt(sq);
+    if (norm > 0.0)
+      for (size_t r = 0; r < g->rows; ++r) gm_row(g, r)[j] /= norm;
+  }
+}
 
 typedef struct { mat inner_left; size_t r_old, r_new; int degenerate; double added; } addrow_res;
 
-/* add_row (isvd.cpp:163-250), reorthogonalize_every = 0 (the default). */
+/* add_row (isvd.cpp:163-250), with the optional periodic re-orthogonalization. */
 static int add_row(isvd_t* st, const double* b, double abs_tol, addrow_res* res) {
   size_t n = st->right.rows, r = st->rank;
   memset(res, 0, sizeof *res);
@@ -740,6 +766,11 @@ static int add_row(isvd_t* st, const double* b, double abs_tol, addrow_res* res)
   res->inner_left = inner.left;
   inner.left.a = NULL;
   st->insertions++;
+  /* isvd.cpp:243-248 */
+  if (st->reorthogonalize_every > 0 && st->insertions % st->reorthogonalize_every == 0) {
+    gm_reorthogonalize(&st->left);
+    orthonormalize_columns(&st->right);
+  }
   mat_free(&top);
   free(last);
   mat_free(&inner.right);
@@ -822,6 +853,12 @@ static void state_free(orc_state* s) {
   free(s->metrics);
   free(s);
 }
+int tko_set_reorthogonalize_every(orc_state* s, int64_t k) {
+  if (k < 0) { set_err("reorthogonalize_every must be nonnegative"); return EINVAL_; }
+  s->isvd.reorthogonalize_every = (size_t)k;
+  return OK;
+}
+
 void tko_destroy(orc_state* s) { state_free(s); }
 
 /* isvd_init validation (isvd.cpp:135-161). */

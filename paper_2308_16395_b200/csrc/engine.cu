@@ -24,6 +24,8 @@
 #include <stdexcept>
 #include <string>
 #include <vector>
+#include <limits>
+#include <cstdio>
 
 #include "../../include/tsg.h"
 #include "kernels.cuh"
@@ -855,12 +857,14 @@ struct tsg_stream {
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
     const bool graph = (s_ == si);
     const int q = mask == 0 ? cur_q : -1;
+    const bool reorth = reorth_every > 0 && (insertions_host + 1) % reorth_every == 0;
     auto body = [&](bool cap) {
       const int saved = cur_q;
       cur_q = q;
       if (s_ != st) wait_ev(s_, ev_proj[par], cap);
       ev_mark(3, s_, cap);
       launch_isvd(B, s_);
+      if (reorth) launch_reorth(ctrl, B.left_new, capr, B.qn, n, s_);
       ev_mark(4, s_, cap);
       record_ev(ev_isvd[par], s_, cap);
       cur_q = saved;
@@ -874,7 +878,8 @@ struct tsg_stream {
                                     (long long)(uintptr_t)evec, (long long)(uintptr_t)pgram,
                                     (long long)(uintptr_t)inner, (long long)(uintptr_t)ipart,
                                     (long long)(uintptr_t)isvd_hand, (long long)(uintptr_t)isvd_gsync,
-                                    n, cap_rows, capr, B.r_hint, d, prof_m0_only() ? -1 : q};
+                                    n, cap_rows, capr, B.r_hint, d, prof_m0_only() ? -1 : q,
+                                    reorth ? 1 : 0};
       for (int k = 0; k + 1 < d; ++k) key.push_back(R[k]);
       run(key, s_, body);
     } else {
@@ -1571,6 +1576,9 @@ struct tsg_stream {
   }
 
   long long cfg_capr = 0, cfg_rows = 0;
+  // ISVDOptions::reorthogonalize_every (isvd.hpp:62-67): MGS of both factors
+  // after every K-th insertion (isvd.cpp:243-248); 0 = off (reference default)
+  long long reorth_every = 0;
 
   void reset_state() {
     free_all();
@@ -1971,11 +1979,12 @@ int tsg_create(const tsg_config* cfg, tsg_stream** out) {
     h->flags = cfg->flags;
     h->cfg_capr = cfg->rank_capacity;
     h->cfg_rows = cfg->row_capacity;
-    if (cfg->reorthogonalize_every != 0) {
-      g_free_err = "reorthogonalize_every > 0 is not supported (reference default is 0)";
+    if (cfg->reorthogonalize_every < 0) {
+      g_free_err = "reorthogonalize_every must be nonnegative";
       delete h;
       return TSG_EINVAL;
     }
+    h->reorth_every = cfg->reorthogonalize_every;
   }
   int st = guarded(h, [&] {
     int n = 0;
@@ -2105,6 +2114,193 @@ int tsg_import_state(tsg_stream* h, const tsg_dims* dims, const double* core,
                      const double* factors, const double* sigma, const double* left,
                      const double* right) {
   return guarded(h, [&] { h->import_state(dims, core, factors, sigma, left, right); });
+}
+
+// ---- TUCKCKPT v1 checkpoints (reference io.cpp:268-423): the streaming
+// state as the reference's save_checkpoint writes it, little-endian:
+//   "TUCKCKPT", u32 version = 1, u32 d, u64 dims[d] (N_0..N_{d-2}, n_d),
+//   u64 ranks[d], f64 tau, u64 mode_order[d] (identity), u32 has_isvd = 1,
+//   f64 core, f64 factors k < d-1 (column-major N_k x R_k), f64 sigma[r],
+//   f64 left (n_d x r, column-major = streaming_factor()), f64 right
+//   (n x r), f64 squared_error, total_input_sq, nonstream_discarded_sq,
+//   u64 n_d.
+// Written to path.tmp and renamed into place (io.cpp:151-191); loading runs
+// load_checkpoint's validation, then from_checkpoint = isvd_init +
+// assemble_streaming_state (coupling re-checked by the import).
+}  // extern "C"
+namespace ckpt {
+constexpr char kMagic[8] = {'T', 'U', 'C', 'K', 'C', 'K', 'P', 'T'};
+constexpr uint32_t kVersion = 1;
+constexpr std::size_t kMaxOrder = 64;
+[[noreturn]] void io_fail(const char* path, const std::string& msg, const char* status) {
+  fail(TSG_EIO, std::string(path) + ": " + msg + " (" + status + ")");
+}
+struct Reader {
+  FILE* f;
+  const char* path;
+  void exact(void* dst, std::size_t n) {
+    if (std::fread(dst, 1, n, f) != n) {
+      if (std::ferror(f)) io_fail(path, "read failed", "io failure");
+      io_fail(path, "file ends before the declared payload", "truncated");
+    }
+  }
+  template <class T>
+  T scalar() {
+    T v;
+    exact(&v, sizeof v);
+    return v;  // little-endian host (x86-64 / aarch64)
+  }
+};
+}  // namespace ckpt
+extern "C" {
+
+int tsg_save_checkpoint(tsg_stream* h, const char* path) {
+  return guarded(h, [&] {
+    if (!h->initialized) fail(TSG_EINVAL, "state not initialised");
+    if (!path) fail(TSG_EINVAL, "save_checkpoint: null path");
+    tsg_dims dm;
+    h->query(&dm);
+    const int d = dm.order;
+    const long long r = dm.rank;
+    long long n = 1, core_n = 1, fac_n = 0;
+    for (int k = 0; k + 1 < d; ++k) {
+      n *= dm.core_dims[k];
+      fac_n += dm.slice_dims[k] * dm.core_dims[k];
+    }
+    for (int k = 0; k < d; ++k) core_n *= dm.core_dims[k];
+    std::vector<double> core(std::max(core_n, 1LL)), fac(std::max(fac_n, 1LL)), sig(std::max(r, 1LL)),
+        left(std::max(dm.n_d * r, 1LL)), right(std::max(n * r, 1LL));
+    h->export_state(core.data(), fac.data(), sig.data(), left.data(), right.data());
+    const std::string tmp = std::string(path) + ".tmp";
+    FILE* f = std::fopen(tmp.c_str(), "wb");
+    if (!f) ckpt::io_fail(path, "cannot open for writing", "io failure");
+    bool ok = true;
+    auto put = [&](const void* p, std::size_t bytes) {
+      if (ok && bytes && std::fwrite(p, 1, bytes, f) != bytes) ok = false;
+    };
+    auto u32 = [&](uint32_t v) { put(&v, 4); };
+    auto u64 = [&](uint64_t v) { put(&v, 8); };
+    auto f64 = [&](double v) { put(&v, 8); };
+    put(ckpt::kMagic, 8);
+    u32(ckpt::kVersion);
+    u32((uint32_t)d);
+    for (int k = 0; k + 1 < d; ++k) u64((uint64_t)dm.slice_dims[k]);
+    u64((uint64_t)dm.n_d);
+    for (int k = 0; k < d; ++k) u64((uint64_t)dm.core_dims[k]);
+    f64(dm.tau);
+    for (int k = 0; k < d; ++k) u64((uint64_t)k);
+    u32(1u);
+    put(core.data(), sizeof(double) * core_n);
+    put(fac.data(), sizeof(double) * fac_n);
+    put(sig.data(), sizeof(double) * r);
+    put(left.data(), sizeof(double) * dm.n_d * r);
+    put(right.data(), sizeof(double) * n * r);
+    f64(dm.squared_error);
+    f64(dm.total_input_sq);
+    f64(dm.nonstream_discarded_sq);
+    u64((uint64_t)dm.n_d);
+    if (std::fflush(f) != 0) ok = false;
+    if (std::fclose(f) != 0) ok = false;
+    if (!ok) {
+      std::remove(tmp.c_str());
+      ckpt::io_fail(path, "write failed", "io failure");
+    }
+    if (std::rename(tmp.c_str(), path) != 0) {
+      std::remove(tmp.c_str());
+      ckpt::io_fail(path, "rename failed", "io failure");
+    }
+  });
+}
+
+int tsg_load_checkpoint(tsg_stream* h, const char* path) {
+  return guarded(h, [&] {
+    if (!path) fail(TSG_EINVAL, "load_checkpoint: null path");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) ckpt::io_fail(path, "cannot open for reading", "io failure");
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    ckpt::Reader rd{f, path};
+    char magic[8];
+    rd.exact(magic, 8);
+    if (std::memcmp(magic, ckpt::kMagic, 8) != 0) ckpt::io_fail(path, "not a model/checkpoint file", "bad magic");
+    const uint32_t ver = rd.scalar<uint32_t>();
+    if (ver != ckpt::kVersion) ckpt::io_fail(path, "unsupported format version " + std::to_string(ver), "bad version");
+    const uint32_t d = rd.scalar<uint32_t>();
+    if (d == 0 || d > ckpt::kMaxOrder)
+      ckpt::io_fail(path, "unreasonable model order " + std::to_string(d), "shape mismatch");
+    std::vector<uint64_t> dims(d), ranks(d), order(d);
+    for (auto& v : dims) v = rd.scalar<uint64_t>();
+    for (auto& v : ranks) v = rd.scalar<uint64_t>();
+    const double tau = rd.scalar<double>();
+    for (auto& v : order) v = rd.scalar<uint64_t>();
+    const uint32_t has_isvd = rd.scalar<uint32_t>();
+    if (has_isvd > 1) ckpt::io_fail(path, "invalid streaming flag", "shape mismatch");
+    auto product = [&](const std::vector<uint64_t>& v) {
+      uint64_t p = 1;
+      for (uint64_t x : v) {
+        if (x == 0 || x > std::numeric_limits<uint64_t>::max() / p)
+          ckpt::io_fail(path, "dimension list has a zero or overflowing entry", "shape mismatch");
+        p *= x;
+      }
+      return p;
+    };
+    const uint64_t core_n = product(ranks);
+    product(dims);
+    if (!(tau > 0.0 && tau < 1.0)) ckpt::io_fail(path, "stored tolerance outside (0, 1)", "shape mismatch");
+    {
+      std::vector<bool> seen(d, false);
+      for (uint64_t m : order) {
+        if (m >= d || seen[m]) ckpt::io_fail(path, "mode order is not a permutation", "shape mismatch");
+        seen[m] = true;
+      }
+    }
+    for (uint32_t k = 0; k < d; ++k)
+      if (ranks[k] > dims[k]) ckpt::io_fail(path, "stored rank exceeds the matching dimension", "shape mismatch");
+    if (has_isvd && d < 2) ckpt::io_fail(path, "streaming checkpoint needs at least two modes", "shape mismatch");
+    // from_checkpoint (io.cpp:414-423): only streaming checkpoints resume
+    if (!has_isvd) fail(TSG_EINVAL, "checkpoint holds a batch model, not a resumable stream");
+    if ((int)d > TSG_MAXD) fail(TSG_EINVAL, "checkpoint order exceeds TSG_MAXD");
+    uint64_t width = 1;
+    for (uint32_t k = 0; k + 1 < d; ++k) width *= ranks[k];
+    const uint64_t r = ranks[d - 1];
+    uint64_t fac_n = 0;
+    for (uint32_t k = 0; k + 1 < d; ++k) fac_n += dims[k] * ranks[k];
+    const uint64_t need = core_n + fac_n + r + dims[d - 1] * r + width * r + 3;
+    {
+      // reject short files before allocating the payload (require_payload)
+      const long here = std::ftell(f);
+      std::fseek(f, 0, SEEK_END);
+      const long end = std::ftell(f);
+      std::fseek(f, here, SEEK_SET);
+      if (here < 0 || end < 0 || (uint64_t)(end - here) < need * 8 + 8)
+        ckpt::io_fail(path, "file ends before the declared payload", "truncated");
+    }
+    std::vector<double> core(core_n), fac(std::max<uint64_t>(fac_n, 1)), sig(std::max<uint64_t>(r, 1)),
+        left(std::max<uint64_t>(dims[d - 1] * r, 1)), right(std::max<uint64_t>(width * r, 1));
+    rd.exact(core.data(), 8 * core_n);
+    rd.exact(fac.data(), 8 * fac_n);
+    rd.exact(sig.data(), 8 * r);
+    rd.exact(left.data(), 8 * dims[d - 1] * r);
+    rd.exact(right.data(), 8 * width * r);
+    tsg_dims dm;
+    std::memset(&dm, 0, sizeof dm);
+    dm.order = (int32_t)d;
+    dm.squared_error = rd.scalar<double>();
+    dm.total_input_sq = rd.scalar<double>();
+    dm.nonstream_discarded_sq = rd.scalar<double>();
+    const uint64_t nd = rd.scalar<uint64_t>();
+    if (nd != dims[d - 1])
+      ckpt::io_fail(path, "slice count does not match the streaming factor height", "shape mismatch");
+    dm.n_d = (int64_t)nd;
+    dm.rank = (int64_t)r;
+    dm.insertions = 0;  // isvd_init starts a fresh insertion count
+    dm.tau = tau;
+    for (uint32_t k = 0; k < d; ++k) dm.core_dims[k] = (int64_t)ranks[k];
+    for (uint32_t k = 0; k + 1 < d; ++k) dm.slice_dims[k] = (int64_t)dims[k];
+    h->import_state(&dm, core.data(), fac.data(), sig.data(), left.data(), right.data());
+  });
 }
 
 double tsg_estimate_relative_error(tsg_stream* h) {

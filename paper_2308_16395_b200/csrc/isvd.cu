@@ -1278,6 +1278,47 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   g_launches += 8;
 }
 
+// Periodic re-orthogonalization (ISVDOptions::reorthogonalize_every,
+// isvd.cpp:243-248): modified Gram-Schmidt over the columns of the streaming
+// factor (GrowableRowMatrix::reorthogonalize, isvd.cpp:102-124) and of the
+// right factor (orthonormalize_columns, linalg.cpp:64-78), in that order.
+// One CTA per matrix: for each column j, the dots with the earlier columns
+// are taken one at a time against the partially updated column (the
+// reference's order); reductions are fixed-order block sums. Element (i, j)
+// lives at a[i * rs + j * cs]; rows = ctrl->n_d (left) or n (right), cols =
+// ctrl->r (both as the insertion left them).
+__global__ void __launch_bounds__(1024) reorth_kernel(const Ctrl* ctrl, double* a, long long rows_fixed,
+                                                       long long rs, long long cs) {
+  __shared__ double scratch[32];
+  const long long rows = rows_fixed > 0 ? rows_fixed : ctrl->n_d;
+  const int cols = ctrl->r;
+  for (int j = 0; j < cols; ++j) {
+    for (int i = 0; i < j; ++i) {
+      double d = 0.0;
+      for (long long r = threadIdx.x; r < rows; r += blockDim.x) d = fma(a[r * rs + i * cs], a[r * rs + j * cs], d);
+      d = block_sum(d, scratch);
+      for (long long r = threadIdx.x; r < rows; r += blockDim.x) a[r * rs + j * cs] -= d * a[r * rs + i * cs];
+      __syncthreads();
+    }
+    double sq = 0.0;
+    for (long long r = threadIdx.x; r < rows; r += blockDim.x) {
+      const double v = a[r * rs + j * cs];
+      sq = fma(v, v, sq);
+    }
+    sq = block_sum(sq, scratch);
+    const double nrm = sqrt(sq);
+    if (nrm > 0.0)
+      for (long long r = threadIdx.x; r < rows; r += blockDim.x) a[r * rs + j * cs] /= nrm;
+    __syncthreads();
+  }
+}
+
+void launch_reorth(const Ctrl* ctrl, double* left, int capr, double* q, long long n, cudaStream_t st) {
+  reorth_kernel<<<1, 1024, 0, st>>>(ctrl, left, 0, capr, 1);
+  reorth_kernel<<<1, 1024, 0, st>>>(ctrl, q, n, 1, n);
+  g_launches += 2;
+}
+
 void launch_zero_slice(Ctrl* ctrl, const SliceCtl* slot, double* left, int capr, RecRing* ring,
                        int order, const long long* spatial, cudaStream_t st) {
   SpatialRanks sr;

@@ -172,6 +172,9 @@ struct IsvdBufs {
   long long spatial_ranks[kMaxD];
 };
 void launch_isvd(const IsvdBufs& b, cudaStream_t st);
+// MGS re-orthogonalization of the streaming factor (row-major, ld capr,
+// ctrl->n_d rows) and of Q (n x ctrl->r): ISVDOptions::reorthogonalize_every.
+void launch_reorth(const Ctrl* ctrl, double* left, int capr, double* q, long long n, cudaStream_t st);
 constexpr int kHandDoubles = 3 * 33 * 33 + 8 * 33 + 16;
 int isvd_inner_scratch(int capr);
 int read_isvd_clocks(long long* out);

@@ -49,6 +49,10 @@ class CouplingDrift(TsgError):
     pass
 
 
+class IoError(TsgError, OSError):
+    """Checkpoint file errors (tucker::IoError, io.hpp:24-33)."""
+
+
 class DeviceError(TsgError):
     pass
 
@@ -60,6 +64,8 @@ def _raise(code: int, msg: str):
         raise CouplingDrift(code, msg)
     if code == 4:
         raise DeviceError(code, msg)
+    if code == 5:
+        raise IoError(code, msg)
     raise TsgError(code, msg)
 
 
@@ -101,7 +107,7 @@ EXPORTED = [
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
     "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
     "tsg_shard_setup", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
-    "tsg_error_sums", "tsg_profile_timeline",
+    "tsg_error_sums", "tsg_profile_timeline", "tsg_save_checkpoint", "tsg_load_checkpoint",
 ]
 
 _LIB = None
@@ -117,6 +123,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
                           "(or __graft_entry__.build()) — there is no CPU fallback")
     L = C.CDLL(path)
     L.tsg_create.argtypes = [C.POINTER(TsgConfig), C.POINTER(C.c_void_p)]
+    L.tsg_save_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
+    L.tsg_load_checkpoint.argtypes = [C.c_void_p, C.c_char_p]
     L.tsg_destroy.argtypes = [C.c_void_p]
     L.tsg_last_error.argtypes = [C.c_void_p]
     L.tsg_last_error.restype = C.c_char_p
@@ -219,12 +227,14 @@ class StreamingState:
     """Owns one device-resident streaming state (a tsg_stream handle)."""
 
     def __init__(self, device: int = 0, asynchronous: bool = False, rank_capacity: int = 0,
-                 row_capacity: int = 0, profile: bool | str = False):
-        """profile: False, True (all phases) or "mode0" (the mode-0 kernel only)."""
+                 row_capacity: int = 0, profile: bool | str = False,
+                 reorthogonalize_every: int = 0):
+        """profile: False, True (all phases) or "mode0" (the mode-0 kernel only).
+        reorthogonalize_every: ISVDOptions (isvd.hpp:62-67), 0 = off."""
         self.L = load_library()
         prof = PROFILE_MODE0 if profile == "mode0" else (PROFILE if profile else 0)
         flags = (ASYNC if asynchronous else 0) | prof
-        cfg = TsgConfig(device, flags, rank_capacity, row_capacity, 0)
+        cfg = TsgConfig(device, flags, rank_capacity, row_capacity, int(reorthogonalize_every))
         h = C.c_void_p()
         code = self.L.tsg_create(C.byref(cfg), C.byref(h))
         if code:
@@ -262,6 +272,10 @@ class StreamingState:
 
     def update_device_ptr(self, ptr: int):
         self._check(self.L.tsg_update(self.h, C.c_void_p(ptr), MEM_DEVICE))
+
+    def save_checkpoint(self, path: str):
+        """save_checkpoint (io.cpp:303-324): TUCKCKPT v1, written atomically."""
+        self._check(self.L.tsg_save_checkpoint(self.h, os.fsencode(path)))
 
     def synchronize(self):
         self._check(self.L.tsg_synchronize(self.h))
@@ -443,9 +457,11 @@ def estimate_relative_error(state: StreamingState) -> float:
     return state.estimate_relative_error()
 
 
-def assemble_streaming_state(st: State, device: int = 0, asynchronous: bool = False) -> StreamingState:
+def assemble_streaming_state(st: State, device: int = 0, asynchronous: bool = False,
+                             reorthogonalize_every: int = 0) -> StreamingState:
     """assemble_streaming_state (streaming.cpp:242-263) from exported pieces."""
-    out = StreamingState(device=device, asynchronous=asynchronous)
+    out = StreamingState(device=device, asynchronous=asynchronous,
+                         reorthogonalize_every=reorthogonalize_every)
     dm = TsgDims()
     dm.order, dm.n_d, dm.rank, dm.insertions = st.order, st.n_d, st.rank, st.insertions
     for k, v in enumerate(st.core_dims):
@@ -462,6 +478,19 @@ def assemble_streaming_state(st: State, device: int = 0, asynchronous: bool = Fa
     out._check(out.L.tsg_import_state(out.h, C.byref(dm), _p(core), _p(fac), _p(sig), _p(left),
                                       _p(right)))
     return out
+
+
+def save_checkpoint(path: str, state: StreamingState) -> None:
+    state.save_checkpoint(path)
+
+
+def load_checkpoint(path: str, device: int = 0, asynchronous: bool = False,
+                    reorthogonalize_every: int = 0) -> StreamingState:
+    """from_checkpoint(load_checkpoint(path)) (io.cpp:326-423) on the device."""
+    st = StreamingState(device=device, asynchronous=asynchronous,
+                        reorthogonalize_every=reorthogonalize_every)
+    st._check(st.L.tsg_load_checkpoint(st.h, os.fsencode(path)))
+    return st
 
 
 def readback_bytes_per_update() -> int:
