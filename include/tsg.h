@@ -166,15 +166,21 @@ int tsg_error_sums(tsg_stream* h, const double* x, int64_t t0, int64_t count,
  * The reference has no distributed mode: this splits ONE stream_update
  * (streaming.hpp:63) across G ranks. Every rank holds the full state (same
  * tsg_init input on every rank, or tsg_import_state of the same state) and
- * rows [bounds[g], bounds[g+1]) of the LAST spatial mode s = d-2 of each
- * slice — a contiguous chunk of the colexicographic slice, passed as a dense
- * tensor N_0 x ... x N_{s-1} x (bounds[g+1]-bounds[g]).
+ * rows [bounds[g], bounds[g+1]) of ONE spatial mode s of each slice, passed
+ * as a dense colexicographic tensor N_0 x .. x (bounds[g+1]-bounds[g]) x ..
+ * x N_{d-2} (a contiguous chunk of the slice when s is the last spatial
+ * mode). tsg_shard_setup picks the largest spatial mode (the last one on
+ * ties); tsg_shard_setup_mode names it (e.g. BASELINE configs[2]: mode 1).
  *
  *   tsg_shard_setup(h, g, G, bounds)            once, after init/import
  *   per slice:
  *     tsg_shard_begin(h, slab, mem_kind, &ex)   local projections of modes < s
  *     while (ex.pending) {
- *       allgather(ex.send -> ex.recv, ex.count doubles per rank, rank order)
+ *       ex.op == TSG_XCHG_ALLGATHER:
+ *         allgather(ex.send -> ex.recv, ex.count doubles per rank, rank order)
+ *       ex.op == TSG_XCHG_ALLREDUCE_SUM:
+ *         recv[i] = sum over ranks of send[i], i < ex.count, the SAME bytes on
+ *         every rank (NCCL allreduce, or a rank-ordered sum)
  *       tsg_shard_continue(h, &ex)
  *     }
  *
@@ -182,17 +188,27 @@ int tsg_error_sums(tsg_stream* h, const double* x, int64_t t0, int64_t count,
  * returned once the local pass is ENQUEUED on tsg_cuda_stream(h): the
  * collective must be enqueued on that stream (or follow a synchronisation),
  * and be complete or enqueued there when tsg_shard_continue is called. In steady state there is exactly one
- * exchange per slice (the compressed local tensor plus partial norms);
- * growth of a basis k < s adds one more. Every reduction over ranks runs in
- * rank order on the gathered bytes, so all ranks end bitwise identical. */
+ * exchange per slice (the compressed local tensor plus partial norms).
+ * Growth of a local basis k < s adds ONE all-reduce of the N_k x N_k partial
+ * Gram of the rank's residual (sthosvd.cpp:45-59 split over the ranks; the
+ * eigensolve runs redundantly, K = W^T E stays local) and one more
+ * compressed-tensor allgather for the modes after k. Every reduction over
+ * ranks runs on identical bytes, so all ranks end bitwise identical. */
+#define TSG_XCHG_ALLGATHER 0
+#define TSG_XCHG_ALLREDUCE_SUM 1
 typedef struct {
-  int32_t pending;   /* 1: an allgather is requested; 0: the update is done */
+  int32_t pending;   /* 1: a collective is requested; 0: the update is done */
+  int32_t op;        /* TSG_XCHG_ALLGATHER or TSG_XCHG_ALLREDUCE_SUM */
   int64_t count;     /* doubles contributed by each rank */
   double* send;      /* device: this rank's count doubles */
-  double* recv;      /* device: world * count doubles, rank g's block at g * count */
+  double* recv;      /* device: allgather: world * count doubles, rank g's block
+                        at g * count; allreduce: count doubles */
 } tsg_exchange;
 
 int tsg_shard_setup(tsg_stream* h, int32_t rank, int32_t world, const int64_t* bounds);
+/* mode: the spatial mode (0 .. d-2) whose rows are split; -1 = the default. */
+int tsg_shard_setup_mode(tsg_stream* h, int32_t rank, int32_t world, int32_t mode,
+                         const int64_t* bounds);
 int tsg_shard_begin(tsg_stream* h, const double* slab, int32_t mem_kind, tsg_exchange* ex);
 int tsg_shard_continue(tsg_stream* h, tsg_exchange* ex);
 

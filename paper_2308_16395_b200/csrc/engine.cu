@@ -343,12 +343,45 @@ struct tsg_stream {
   long long launches_at_create = 0;
 
   // ------------------------------------------------------------ memory
+  // Freed blocks up to kPoolBlockMax are kept (by capacity) and handed out
+  // again: the growth path allocates the same temporaries for every basis
+  // growth, and cudaMalloc / cudaFree cost 0.1-1 ms each and synchronise the
+  // device. dfree() drains the engine's streams before it caches a block
+  // (what cudaFree's implicit synchronisation guaranteed before).
+  static constexpr long long kPoolBlockMax = 256LL << 20;
+  static constexpr long long kPoolTotalMax = 2048LL << 20;
+  std::multimap<long long, void*> pool;  // capacity in bytes -> block
+  std::map<void*, long long> pool_cap;   // every live or pooled block: its capacity
+  long long pool_bytes = 0;
+  void pool_flush() {
+    for (auto& kv : pool) {
+      pool_cap.erase(kv.second);
+      cudaFree(kv.second);
+    }
+    pool.clear();
+    pool_bytes = 0;
+  }
   double* dalloc(long long n_doubles) {
     if (n_doubles <= 0) n_doubles = 1;
+    const long long bytes = n_doubles * (long long)sizeof(double);
     void* p = nullptr;
-    ck(cudaMalloc(&p, n_doubles * sizeof(double)), "cudaMalloc");
-    allocs.emplace_back(p, n_doubles * (long long)sizeof(double));
-    cur_bytes += n_doubles * (long long)sizeof(double);
+    auto it = pool.lower_bound(bytes);
+    if (it != pool.end() && it->first <= bytes + bytes / 4 + 4096) {
+      p = it->second;
+      pool_bytes -= it->first;
+      pool.erase(it);
+    } else {
+      cudaError_t e = cudaMalloc(&p, bytes);
+      if (e == cudaErrorMemoryAllocation && !pool.empty()) {
+        cudaGetLastError();
+        pool_flush();
+        e = cudaMalloc(&p, bytes);
+      }
+      ck(e, "cudaMalloc");
+      pool_cap[p] = bytes;
+    }
+    allocs.emplace_back(p, bytes);
+    cur_bytes += bytes;
     peak_bytes = std::max(peak_bytes, cur_bytes);
     return static_cast<double*>(p);
   }
@@ -360,6 +393,18 @@ struct tsg_stream {
         allocs.erase(allocs.begin() + i);
         break;
       }
+    auto c = pool_cap.find(p);
+    if (c != pool_cap.end() && c->second <= kPoolBlockMax &&
+        pool_bytes + c->second <= kPoolTotalMax && st && si) {
+      if (sc) cudaStreamSynchronize(sc);
+      if (s2) cudaStreamSynchronize(s2);
+      cudaStreamSynchronize(si);
+      cudaStreamSynchronize(st);
+      pool.emplace(c->second, p);
+      pool_bytes += c->second;
+      return;
+    }
+    if (c != pool_cap.end()) pool_cap.erase(c);
     cudaFree(p);
   }
   void free_all() {
@@ -369,6 +414,10 @@ struct tsg_stream {
     if (s2) cudaStreamSynchronize(s2);
     for (auto& a : allocs) cudaFree(a.first);
     allocs.clear();
+    for (auto& kv : pool) cudaFree(kv.second);
+    pool.clear();
+    pool_cap.clear();
+    pool_bytes = 0;
     cur_bytes = 0;
     for (auto& kv : graphs) {
       cudaGraphExecDestroy(kv.second.exec);
@@ -589,6 +638,32 @@ struct tsg_stream {
     s.owned.clear();
   }
 
+  // Gram route of mode_subspace from a formed Gram matrix (sthosvd.cpp:61-75):
+  // eigensolve, truncation against delta, basis = leading eigenvectors. The
+  // sharded growth calls it on the all-reduced sum of the ranks' partial Grams.
+  void subspace_from_gram(Sub& s, const double* g, long long rows, double delta,
+                          long long* rk_d = nullptr) {
+    if (!rk_d) {
+      rk_d = reinterpret_cast<long long*>(dalloc(2));
+      s.owned.push_back(reinterpret_cast<double*>(rk_d));
+    }
+    double* disc_d = reinterpret_cast<double*>(rk_d) + 1;
+    double* work = dalloc(3 * rows * rows + 512);
+    double* vec = dalloc(rows * rows);
+    double* ev = dalloc(rows);
+    s.owned.insert(s.owned.end(), {work, vec, ev});
+    launch_sym_eig(g, (int)rows, ev, vec, work, nullptr, st);
+    launch_truncate(ev, (int)rows, delta, 0, rk_d, disc_d, st);
+    long long hr[2];
+    ck(cudaMemcpyAsync(hr, rk_d, 16, cudaMemcpyDeviceToHost, st), "rank D2H");
+    sync();
+    ck(cudaGetLastError(), "mode_subspace");
+    s.rank = hr[0];
+    std::memcpy(&s.disc, &hr[1], 8);
+    s.basis = vec;
+    s.evals = ev;
+  }
+
   // mode_subspace (sthosvd.cpp:39-92) on a device tensor.
   Sub mode_subspace(const double* t, const long long* dims, int order, int mode, double delta) {
     Sub s;
@@ -611,21 +686,9 @@ struct tsg_stream {
       double* g = dalloc(rows * rows);
       const int splits = gram_splits((int)rows, cols);
       double* part = dalloc((long long)splits * rows * rows);
-      double* work = dalloc(3 * rows * rows + 512);
-      double* vec = dalloc(rows * rows);
-      double* ev = dalloc(rows);
-      s.owned.insert(s.owned.end(), {g, part, work, vec, ev});
+      s.owned.insert(s.owned.end(), {g, part});
       launch_gram(A, (int)rows, cols, g, part, st);
-      launch_sym_eig(g, (int)rows, ev, vec, work, nullptr, st);
-      launch_truncate(ev, (int)rows, delta, 0, rk_d, disc_d, st);
-      long long hr[2];
-      ck(cudaMemcpyAsync(hr, rk_d, 16, cudaMemcpyDeviceToHost, st), "rank D2H");
-      sync();
-      ck(cudaGetLastError(), "mode_subspace");
-      s.rank = hr[0];
-      std::memcpy(&s.disc, &hr[1], 8);
-      s.basis = vec;
-      s.evals = ev;
+      subspace_from_gram(s, g, rows, delta, rk_d);
       return s;
     }
     // thin route
@@ -705,14 +768,25 @@ struct tsg_stream {
   // `dst` (concat of p and the carried coefficients), yd updated.
   void expand_mode(const double* y, long long* yd, int mode, double delta, double* p,
                    double* dst) {
+    expand_residual(y, yd, mode, p);
+    Sub s = mode_subspace(ebuf, yd, d - 1, mode, delta);
+    dbg("expand: mode_subspace");
+    expand_finish(yd, mode, s, p, dst);
+  }
+  // First half: P = U^T Y into p, residual E = Y - U P into ebuf.
+  void expand_residual(const double* y, const long long* yd, int mode, double* p) {
     if (!ebuf) ebuf = dalloc(slice_elems);
     if (!kbuf) kbuf = dalloc(slice_elems);
-    ModeView v{prod(yd, mode), yd[mode], prod(yd + mode + 1, d - 2 - mode)};
     dbg("expand: entry");
     project(y, yd, mode, p, partial + 2LL * kMaxGrid * kMaxD, ebuf);
     dbg("expand: residual");
-    Sub s = mode_subspace(ebuf, yd, d - 1, mode, delta);
-    dbg("expand: mode_subspace");
+  }
+  // Second half, from the subspace W of the residual: carried = W^T E,
+  // U <- [U W], core / Q padded, ledger, dst = concat(P, carried). On a
+  // sharded rank y / p / ebuf are the local parts and the state updates run
+  // identically on every rank.
+  void expand_finish(long long* yd, int mode, Sub& s, double* p, double* dst) {
+    ModeView v{prod(yd, mode), yd[mode], prod(yd + mode + 1, d - 2 - mode)};
     const long long g = s.rank;
     if (R[mode] + g > N[mode]) fail(TSG_EOTHER, "expansion exceeds the mode size");
     // carried = W^T E (streaming.cpp:145)
@@ -1125,8 +1199,11 @@ struct tsg_stream {
   // of mode m0_in with dims yd_in: rebuild the input of mode `em` (the first
   // mode whose residual exceeds delta), grow it, continue with the grown
   // tensor, then insert. Slot `par` holds the slice's decision record.
+  // `commit_lo` / `with_total` / `mask0`: the sharded engine enters here after
+  // local modes [0, commit_lo) were committed (and some of them grown) already.
   void run_growth(const double* base_in, const long long* yd_in, int m0_in, int em, double delta,
-                  int par, std::chrono::steady_clock::time_point t0) {
+                  int par, std::chrono::steady_clock::time_point t0, int commit_lo = 0,
+                  int with_total = 1, int mask0 = 0) {
     long long yd[kMaxD];
     for (int k = 0; k + 1 < d; ++k) yd[k] = yd_in[k];
     DecideArgs da;
@@ -1137,8 +1214,8 @@ struct tsg_stream {
     da.order = d;
     da.partial = partial;
     const double* base = base_in;
-    int m0 = m0_in, mask = 0;
-    launch_commit_modes(ctrl, slots + par, 0, em, 1, st);
+    int m0 = m0_in, mask = mask0;
+    launch_commit_modes(ctrl, slots + par, commit_lo, em, with_total, st);
     const double* b = nullptr;
     while (true) {
       // rebuild the input of mode em from `base` (same kernels, same data)
@@ -1192,39 +1269,62 @@ struct tsg_stream {
 
   // ------------------------------------------------------ sharded update
   // SURVEY §8(e). Rank `shard_rank` of `shard_world` holds rows
-  // [shard_lo[g], shard_lo[g] + shard_n[g]) of the last spatial mode
-  // s = d-2 of every slice (a contiguous chunk of the colexicographic slice).
-  // Modes 0..s-1 are projected on the local slab; the exchange is ONE
-  // allgather of [partial norm pairs of modes < s | local part of the input
-  // of mode s] (the compressed tensor, R_0..R_{s-1} x N_s/G doubles per rank).
+  // [shard_lo[g], shard_lo[g] + shard_n[g]) of ONE spatial mode s of every
+  // slice (tsg_shard_setup_mode; default: the largest spatial mode, the last
+  // one on ties), as a dense tensor N_0 x .. x n_g x .. x N_{d-2}. Modes
+  // 0..s-1 are projected on the local slab; the per-slice exchange is ONE
+  // allgather of [partial norm pairs of the local modes | local part of the
+  // input of mode s] (the compressed tensor R_0..R_{s-1} x n_g x N_{s+1}..).
   // Mode s onwards, the decision and the insertion then run redundantly on
   // the identical assembled bytes, so all ranks hold bitwise-identical states
-  // without a factor broadcast. Basis growth at a mode k < s (rare) gathers
-  // the input of mode k the same way and grows redundantly.
-  // The host fulfils each exchange (NCCL allgather over NVLink, or any other
-  // transport) between tsg_shard_begin and tsg_shard_continue.
-  int shard_world = 0, shard_rank = 0;
+  // without a factor broadcast.
+  // Basis growth at a local mode k < s: every rank forms the N_k x N_k Gram of
+  // ITS part of the residual, ONE all-reduce sums the partial Grams
+  // (N_k^2 doubles; identical bytes on every rank), the eigensolve and the
+  // truncation run redundantly, and K = W^T E, the concat and the remaining
+  // local modes stay local (sthosvd.cpp:45-59, streaming.cpp:142-151 split
+  // over the ranks). The thin route (N_k > columns, tiny tensors only) falls
+  // back to gathering the mode's input.
+  // The host fulfils each exchange (NCCL over NVLink, or any other transport)
+  // between tsg_shard_begin and tsg_shard_continue.
+  int shard_world = 0, shard_rank = 0, shard_mode = -1;
   long long shard_lo[kMaxShards] = {0}, shard_n[kMaxShards] = {0};
   double *sh_send = nullptr, *sh_recv = nullptr, *sh_z = nullptr, *sh_stage = nullptr;
-  long long sh_send_cap = 0, sh_recv_cap = 0, sh_stage_cap = 0;
-  const double* sh_y = nullptr;  // this slice's local slab (device)
-  int sh_phase = 0;              // 0 idle, 1 mode-s input gather, 2 growth-mode input gather
+  double *sh_loc = nullptr, *sh_p = nullptr, *sh_gpart = nullptr, *sh_unf = nullptr;
+  long long sh_send_cap = 0, sh_recv_cap = 0, sh_stage_cap = 0, sh_loc_cap = 0, sh_p_cap = 0,
+            sh_gpart_cap = 0, sh_unf_cap = 0;
+  const double* sh_y = nullptr;     // this slice's local slab (device)
+  const double* sh_base = nullptr;  // local input of mode sh_m0 (the slab, or the grown local tensor)
+  int sh_m0 = 0;                    // first local mode not yet settled for this slice
+  int sh_mask = 0;                  // modes grown so far for this slice
+  bool sh_total_done = false;       // the slice's ||y||^2 is booked
+  // 0 idle, 1 compressed-tensor gather, 2 growth-mode input gather (thin
+  // route), 3 partial-Gram all-reduce
+  int sh_phase = 0;
   int sh_em = -1, sh_header = 0;
   long long sh_count = 0;
+  long long sh_yd[kMaxD] = {0};     // local dims of the tensor behind sh_p / ebuf (phase 3)
   std::chrono::steady_clock::time_point sh_t0;
 
-  void shard_setup(int rank, int world, const long long* bounds) {
+  void shard_setup(int rank, int world, int mode, const long long* bounds) {
     if (!initialized) fail(TSG_EINVAL, "shard_setup: state not initialised");
     if (world < 1 || world > kMaxShards || rank < 0 || rank >= world)
       fail(TSG_EINVAL, "shard_setup: bad rank / world size");
-    const long long ns = N[d - 2];
+    if (mode < -1 || mode > d - 2) fail(TSG_EINVAL, "shard_setup: the shard mode must be a spatial mode");
+    if (mode < 0) {
+      mode = 0;
+      for (int k = 1; k + 1 < d; ++k)
+        if (N[k] >= N[mode]) mode = k;  // largest spatial mode, the last one on ties
+    }
+    const long long ns = N[mode];
     if (bounds[0] != 0 || bounds[world] != ns)
-      fail(TSG_EINVAL, "shard_setup: bounds must cover [0, N_s) of the last spatial mode");
+      fail(TSG_EINVAL, "shard_setup: bounds must cover [0, N_s) of the shard mode");
     for (int g = 0; g < world; ++g)
       if (bounds[g + 1] <= bounds[g]) fail(TSG_EINVAL, "shard_setup: every rank needs >= 1 row");
     flush();
     shard_world = world;
     shard_rank = rank;
+    shard_mode = mode;
     for (int g = 0; g < world; ++g) {
       shard_lo[g] = bounds[g];
       shard_n[g] = bounds[g + 1] - bounds[g];
@@ -1236,49 +1336,69 @@ struct tsg_stream {
     for (int g = 0; g < shard_world; ++g) m = std::max(m, shard_n[g]);
     return m;
   }
-  void shard_buffers(long long count) {
+  void shard_buffers(long long count, long long recv_count) {
     if (count > sh_send_cap) {
       dfree(sh_send);
       sh_send = dalloc(count);
       sh_send_cap = count;
     }
-    if (count * shard_world > sh_recv_cap) {
+    if (recv_count > sh_recv_cap) {
       dfree(sh_recv);
-      sh_recv = dalloc(count * shard_world);
-      sh_recv_cap = count * shard_world;
+      sh_recv = dalloc(recv_count);
+      sh_recv_cap = recv_count;
     }
   }
-  // Project the local slab through modes [0, m_end); the last output (the
-  // slab itself when m_end == 0) lands in sh_send + header, the per-mode
-  // partial pairs (when header > 0) in sh_send[0, 2 m_end).
-  void shard_local_pass(int m_end, int header) {
+  void ensure_buf(double*& buf, long long& cap, long long need) {
+    if (need <= cap) return;
+    dfree(buf);
+    buf = dalloc(need);
+    cap = need;
+  }
+  // Local dims of the tensor that enters local mode `m` (modes < m compressed).
+  void shard_local_dims(int m, long long* yd) const {
+    for (int k = 0; k + 1 < d; ++k) yd[k] = k < m ? R[k] : N[k];
+    yd[shard_mode] = shard_n[shard_rank];
+  }
+  // Elements per shard-mode row of the input of mode `m` (m <= s): what one
+  // row of a rank's block carries in an exchange of that tensor.
+  long long shard_row_elems(int m) const {
+    long long e = 1;
+    for (int k = 0; k + 1 < d; ++k)
+      if (k != shard_mode) e *= k < m ? R[k] : N[k];
+    return e;
+  }
+  // Project the local tensor `base` (the input of local mode m_begin) through
+  // modes [m_begin, m_end); the last output (base itself when the range is
+  // empty) lands in sh_send + header, the partial pairs of those modes (when
+  // header > 0) in sh_send[0, 2 (m_end - m_begin)).
+  void shard_local_pass(const double* base, int m_begin, int m_end, int header) {
     long long yd[kMaxD];
-    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
-    yd[d - 2] = shard_n[shard_rank];
+    shard_local_dims(m_begin, yd);
     ShardPairs sp;
     std::memset(&sp, 0, sizeof sp);
     sp.partial = partial;
-    sp.nmodes = m_end;
-    const double* cur = sh_y;
+    sp.nmodes = m_end - m_begin;
+    const double* cur = base;
     int off = 0;
-    for (int k = 0; k < m_end; ++k) {
-      double* out = (k == m_end - 1) ? sh_send + header : pick(cur, nullptr);
-      sp.off[k] = off;
-      sp.cnt[k] = project(cur, yd, k, out, partial + off);
-      off += 2 * sp.cnt[k];
+    for (int k = m_begin; k < m_end; ++k) {
+      double* out = (k == m_end - 1) ? sh_send + header : pick(cur, base);
+      sp.off[k - m_begin] = off;
+      sp.cnt[k - m_begin] = project(cur, yd, k, out, partial + off);
+      off += 2 * sp.cnt[k - m_begin];
       yd[k] = R[k];
       cur = out;
     }
-    if (m_end == 0)
-      ck(cudaMemcpyAsync(sh_send + header, sh_y, sizeof(double) * prod(yd, d - 1),
+    if (m_end == m_begin)
+      ck(cudaMemcpyAsync(sh_send + header, base, sizeof(double) * prod(yd, d - 1),
                          cudaMemcpyDeviceToDevice, st), "slab copy");
     if (header > 0) launch_shard_pack_pairs(sp, sh_send, st);
   }
   // The request is returned as soon as the local pass is enqueued: the
   // caller's collective must run on tsg_cuda_stream(h) (or after a sync).
-  void shard_request(tsg_exchange* ex) {
+  void shard_request(tsg_exchange* ex, int op) {
     ck(cudaGetLastError(), "shard local pass");
     ex->pending = 1;
+    ex->op = op;
     ex->count = sh_count;
     ex->send = sh_send;
     ex->recv = sh_recv;
@@ -1296,9 +1416,21 @@ struct tsg_stream {
     }
     r_exact = ctrl_h->r;
     ex->pending = 0;
+    ex->op = TSG_XCHG_ALLGATHER;
     ex->count = 0;
     ex->send = ex->recv = nullptr;
     check_status();
+  }
+  // Phase 1 request: local modes [sh_m0, s) of sh_base, then the allgather of
+  // [pairs of those modes | compressed local tensor].
+  void shard_request_compressed(tsg_exchange* ex) {
+    const int s = shard_mode;
+    sh_header = 2 * (s - sh_m0);
+    sh_count = (sh_header + shard_row_elems(s) * shard_max_n() + 1) / 2 * 2;
+    shard_buffers(sh_count, sh_count * shard_world);
+    shard_local_pass(sh_base, sh_m0, s, sh_header);
+    sh_phase = 1;
+    shard_request(ex, TSG_XCHG_ALLGATHER);
   }
 
   void shard_begin(const double* slab, int mem_kind, tsg_exchange* ex) {
@@ -1307,15 +1439,10 @@ struct tsg_stream {
     if (sh_phase != 0) fail(TSG_EINVAL, "tsg_shard_begin: the previous slice's exchange is pending");
     if (have_prev || !pending.empty()) flush();  // a preceding async tsg_update
     sh_t0 = std::chrono::steady_clock::now();
-    const int s = d - 2;
-    const long long le = prod(N, s) * shard_n[shard_rank];
+    const long long le = slice_elems / N[shard_mode] * shard_n[shard_rank];
     const bool misaligned = (reinterpret_cast<uintptr_t>(slab) & 15) != 0;
     if (mem_kind == TSG_MEM_HOST || misaligned) {
-      if (le > sh_stage_cap) {
-        dfree(sh_stage);
-        sh_stage = dalloc(le);
-        sh_stage_cap = le;
-      }
+      ensure_buf(sh_stage, sh_stage_cap, le);
       ck(cudaMemcpyAsync(sh_stage, slab, sizeof(double) * le,
                          mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
                          st), "slab copy");
@@ -1323,45 +1450,110 @@ struct tsg_stream {
     } else {
       sh_y = slab;
     }
-    sh_header = 2 * s;
-    sh_count = (sh_header + prod(R, s) * shard_max_n() + 1) / 2 * 2;
-    shard_buffers(sh_count);
-    shard_local_pass(s, sh_header);
-    sh_phase = 1;
-    shard_request(ex);
+    sh_base = sh_y;
+    sh_m0 = 0;
+    sh_mask = 0;
+    sh_total_done = false;
+    shard_request_compressed(ex);
+  }
+
+  ShardLayout shard_layout() const {
+    ShardLayout L;
+    std::memset(&L, 0, sizeof L);
+    L.world = shard_world;
+    L.count = sh_count;
+    L.ns = N[shard_mode];
+    for (int g = 0; g < shard_world; ++g) {
+      L.lo[g] = shard_lo[g];
+      L.nloc[g] = shard_n[g];
+    }
+    return L;
+  }
+
+  // Local-mode growth, first half: the local residual of mode em and its
+  // partial Gram; the all-reduce request.
+  void shard_growth_request(int em, tsg_exchange* ex) {
+    const long long rows = N[em];
+    long long yd[kMaxD];
+    shard_local_dims(sh_m0, yd);
+    const double* cur = sh_base;
+    for (int k = sh_m0; k < em; ++k) {
+      double* out = pick(cur, sh_base);
+      project(cur, yd, k, out, partial + 2LL * kMaxGrid * kMaxD);
+      yd[k] = R[k];
+      cur = out;
+    }
+    const long long size = prod(yd, d - 1);
+    ensure_buf(sh_p, sh_p_cap, size / rows * std::max(R[em], 1LL));
+    expand_residual(cur, yd, em, sh_p);  // P_loc -> sh_p, E_loc -> ebuf
+    std::memcpy(sh_yd, yd, sizeof yd);
+    const long long cols = size / rows;
+    const double* A = ebuf;
+    if (em != 0) {
+      ensure_buf(sh_unf, sh_unf_cap, size);
+      ModeView v{prod(yd, em), rows, prod(yd + em + 1, d - 2 - em)};
+      launch_unfold(ebuf, v, sh_unf, st);
+      A = sh_unf;
+    }
+    sh_count = (rows * rows + 1) / 2 * 2;
+    shard_buffers(sh_count, sh_count);
+    const int splits = gram_splits((int)rows, cols);
+    ensure_buf(sh_gpart, sh_gpart_cap, (long long)splits * rows * rows);
+    if (sh_count > rows * rows)
+      ck(cudaMemsetAsync(sh_send + rows * rows, 0, sizeof(double), st), "memset");
+    launch_gram(A, (int)rows, cols, sh_send, sh_gpart, st);
+    sh_em = em;
+    sh_phase = 3;
+    shard_request(ex, TSG_XCHG_ALLREDUCE_SUM);
   }
 
   void shard_continue(tsg_exchange* ex) {
     if (sh_phase == 0) fail(TSG_EINVAL, "tsg_shard_continue: no exchange pending");
-    const int s = d - 2, G = shard_world;
-    ShardLayout L;
-    std::memset(&L, 0, sizeof L);
-    L.world = G;
-    L.count = sh_count;
-    for (int g = 0; g < G; ++g) {
-      L.lo[g] = shard_lo[g];
-      L.nloc[g] = shard_n[g];
-    }
+    const int s = shard_mode, G = shard_world;
     long long yd[kMaxD];
-    for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
-    if (sh_phase == 2) {
-      // the gathered input of the growing mode: grow redundantly from it
+    if (sh_phase == 3) {
+      // the summed Gram of the residual: subspace, then everything local
       const int em = sh_em;
-      L.header = 0;
-      L.inner = prod(R, em) * prod(N + em, s - em);
-      launch_shard_unpack(L, sh_recv, sh_z, nullptr, st);
-      for (int k = 0; k < em; ++k) yd[k] = R[k];
       pull_ctrl();
-      run_growth(sh_z, yd, em, em, slots_h[0].delta, 0, sh_t0);
+      Sub sub;
+      subspace_from_gram(sub, sh_recv, N[em], slots_h[0].delta);
+      long long ydl[kMaxD];
+      std::memcpy(ydl, sh_yd, sizeof ydl);
+      const long long grown = prod(ydl, d - 1) / N[em] * (R[em] + sub.rank);
+      ensure_buf(sh_loc, sh_loc_cap, grown);
+      // sh_base may be sh_loc itself (a second local growth): the concat
+      // reads only sh_p and kbuf
+      expand_finish(ydl, em, sub, sh_p, sh_loc);
+      sh_mask |= 1 << em;
+      sh_base = sh_loc;
+      sh_m0 = em + 1;
+      shard_request_compressed(ex);
+      return;
+    }
+    if (sh_phase == 2) {
+      // thin route: the gathered input of the growing mode, grown redundantly
+      const int em = sh_em;
+      ShardLayout L = shard_layout();
+      L.header = 0;
+      L.inner = 1;
+      for (int k = 0; k < s; ++k) L.inner *= k < em ? R[k] : N[k];
+      L.outer = prod(N + s + 1, d - 2 - s);
+      launch_shard_unpack(L, sh_recv, sh_z, nullptr, st);
+      for (int k = 0; k + 1 < d; ++k) yd[k] = k < em ? R[k] : N[k];
+      pull_ctrl();
+      run_growth(sh_z, yd, em, em, slots_h[0].delta, 0, sh_t0, em, 0, sh_mask);
       shard_done(ex);
       return;
     }
     // phase 1: assemble the input of mode s and the per-rank pairs of the
-    // local modes (into the decision's partial area, rank order)
+    // local modes [m0, s) (into the decision's partial area, rank order)
+    const int m0 = sh_m0;
+    ShardLayout L = shard_layout();
     L.header = sh_header;
     L.inner = prod(R, s);
+    L.outer = prod(N + s + 1, d - 2 - s);
     launch_shard_unpack(L, sh_recv, sh_z, partial, st);
-    for (int k = 0; k < s; ++k) yd[k] = R[k];
+    for (int k = 0; k + 1 < d; ++k) yd[k] = k < s ? R[k] : N[k];
     DecideArgs da;
     std::memset(&da, 0, sizeof da);
     da.slot = slots;
@@ -1369,10 +1561,10 @@ struct tsg_stream {
     da.tau = tau;
     da.order = d;
     da.partial = partial;
-    da.first_mode = 0;
-    int off = 2 * G * s;
-    for (int k = 0; k < s; ++k) {
-      da.off[k] = 2 * G * k;
+    da.first_mode = m0;
+    int off = 2 * G * (s - m0);
+    for (int k = m0; k < s; ++k) {
+      da.off[k] = 2 * G * (k - m0);
       da.cnt[k] = G;
     }
     long long ydk[kMaxD];
@@ -1386,31 +1578,63 @@ struct tsg_stream {
       ydk[k] = R[k];
       cur = out;
     }
-    // the decision comes back through the mapped slot (a spin, no copy call)
-    da.host_slot = hslot_d;
-    da.seq_counter = seq_dev;
-    ++seq_expect[0];
-    launch_decide(da, st);
-    const SliceCtl sc = wait_slot(0);
-    slots_h[0] = sc;  // run_growth reads the delta of a local-mode growth from here
+    SliceCtl sc;
+    if (m0 == 0) {
+      // the decision comes back through the mapped slot (a spin, no copy call)
+      da.host_slot = hslot_d;
+      da.seq_counter = seq_dev;
+      ++seq_expect[0];
+      launch_decide(da, st);
+      sc = wait_slot(0);
+      slots_h[0] = sc;  // the growth paths read the slice's delta from here
+    } else {
+      // after a local growth: the remaining modes against the slice's delta
+      launch_decide(da, st);
+      pull_slot(0);
+      sc = slots_h[0];
+    }
+    const int with_total = sh_total_done ? 0 : 1;
     if (sc.zero_slice) {
       zero_slice_path(0, sh_t0);
     } else if (sc.expand_mode < 0) {
-      enqueue_isvd(cur, 0, 0, st, true, sh_t0);
+      if (m0 == 0) {
+        enqueue_isvd(cur, 0, 0, st, true, sh_t0);
+      } else {
+        launch_commit_modes(ctrl, slots, m0, d - 1, with_total, st);
+        pull_ctrl();
+        r_exact = ctrl_h->r;
+        ensure_pipe();
+        enqueue_isvd(cur, 0, sh_mask, st, false, sh_t0);
+      }
     } else if (sc.expand_mode >= s) {
       pull_ctrl();
-      run_growth(sh_z, yd, s, sc.expand_mode, sc.delta, 0, sh_t0);
+      run_growth(sh_z, yd, s, sc.expand_mode, sc.delta, 0, sh_t0, m0, with_total, sh_mask);
     } else {
-      // growth at a local mode: gather that mode's input, grow redundantly
-      sh_em = sc.expand_mode;
-      sh_count = (prod(R, sh_em) * prod(N + sh_em, s - sh_em) * shard_max_n() + 1) / 2 * 2;
-      shard_buffers(sh_count);
-      shard_local_pass(sh_em, 0);
-      sh_phase = 2;
-      shard_request(ex);
+      // growth at a local mode
+      const int em = sc.expand_mode;
+      launch_commit_modes(ctrl, slots, m0, em, with_total, st);
+      sh_total_done = true;
+      const long long cols_full = slice_elems_at(em) / N[em];
+      if (N[em] <= cols_full) {
+        shard_growth_request(em, ex);
+      } else {
+        // thin route (rows > columns): gather that mode's input instead
+        sh_em = em;
+        sh_count = (shard_row_elems(em) * shard_max_n() + 1) / 2 * 2;
+        shard_buffers(sh_count, sh_count * shard_world);
+        shard_local_pass(sh_base, sh_m0, em, 0);
+        sh_phase = 2;
+        shard_request(ex, TSG_XCHG_ALLGATHER);
+      }
       return;
     }
     shard_done(ex);
+  }
+  // Elements of the full input tensor of mode m (modes < m compressed).
+  long long slice_elems_at(int m) const {
+    long long e = 1;
+    for (int k = 0; k + 1 < d; ++k) e *= k < m ? R[k] : N[k];
+    return e;
   }
 
   void flush() {
@@ -2051,11 +2275,16 @@ int tsg_error_sums(tsg_stream* h, const double* x, int64_t t0, int64_t count, in
 }
 
 int tsg_shard_setup(tsg_stream* h, int32_t rank, int32_t world, const int64_t* bounds) {
+  return tsg_shard_setup_mode(h, rank, world, -1, bounds);
+}
+
+int tsg_shard_setup_mode(tsg_stream* h, int32_t rank, int32_t world, int32_t mode,
+                         const int64_t* bounds) {
   return guarded(h, [&] {
     if (!bounds) fail(TSG_EINVAL, "tsg_shard_setup: bounds must not be null");
     if (world < 1 || world > kMaxShards) fail(TSG_EINVAL, "tsg_shard_setup: bad world size");
     std::vector<long long> b(bounds, bounds + world + 1);
-    h->shard_setup(rank, world, b.data());
+    h->shard_setup(rank, world, mode, b.data());
   });
 }
 

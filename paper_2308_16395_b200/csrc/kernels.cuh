@@ -216,13 +216,15 @@ struct ShardPairs {
 // out[2k], out[2k+1] = (sum res_sq, sum x_sq) of mode k, fixed order.
 void launch_shard_pack_pairs(const ShardPairs& p, double* out, cudaStream_t st);
 // Gathered buffer: rank g's block starts at g * count and holds `header`
-// doubles of pairs, then inner * nloc[g] doubles of its chunk, which lands
-// at z + inner * lo[g]. pairs_out (may be null) receives the pairs grouped
-// per mode: [k * 2 * world + 2 g + j].
+// doubles of pairs, then its part of the tensor, inner x nloc[g] x outer
+// (rows [lo[g], lo[g] + nloc[g]) of the shard mode, which has ns rows in
+// all): element (i, j, o) lands at z[i + inner * (lo[g] + j + ns * o)].
+// pairs_out (may be null) receives the pairs grouped per mode:
+// [k * 2 * world + 2 g + j].
 struct ShardLayout {
   int world;
   int header;
-  long long count, inner;
+  long long count, inner, outer, ns;
   long long lo[kMaxShards], nloc[kMaxShards];
 };
 void launch_shard_unpack(const ShardLayout& L, const double* recv, double* z, double* pairs_out,

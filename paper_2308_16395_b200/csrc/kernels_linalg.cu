@@ -520,8 +520,9 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int rows,
   }
 }
 
-// Small Grams with many K splits: one warp per (upper) element, lanes take
-// the splits strided by 32, then a fixed butterfly (deterministic order).
+// Small Grams with many K splits: one warp per element of the full square
+// (each sums its upper-triangle mirror, so G is symmetric bit for bit), lanes
+// take the splits strided by 32, then a fixed butterfly (deterministic order).
 __global__ void gram_reduce_warp_kernel(const double* __restrict__ partial, int rows, int splits,
                                         double* __restrict__ g) {
   const long long total = (long long)rows * rows;
@@ -732,7 +733,8 @@ int gram_splits(int rows, long long cols) {
   const int tiles = nt * (nt + 1) / 2;
   static const long long waves = [] {  // TSG_GRAM_WAVES: CTAs per SM targeted
     const char* e = std::getenv("TSG_GRAM_WAVES");
-    return e ? std::atoll(e) : 8LL;
+    const long long w = e ? std::atoll(e) : 8LL;
+    return w < 1 ? 1LL : (w > 64 ? 64LL : w);
   }();
   long long s = (waves * kNumSMs + tiles - 1) / tiles;
   const long long max_by_cols = (cols + 4 * GK - 1) / (4 * GK);
@@ -740,7 +742,7 @@ int gram_splits(int rows, long long cols) {
   // narrow modes need many CTAs to keep enough bytes in flight; the partial
   // buffer (splits x rows^2) stays <= 32 Mi doubles
   long long cap = (1LL << 25) / ((long long)rows * rows);
-  if (cap < 256) cap = 256;
+  if (cap < 1) cap = 1;
   if (cap > 4096) cap = 4096;
   if (s > cap) s = cap;
   if (s < 1) s = 1;

@@ -1,8 +1,8 @@
 // Kernels of the sharded streaming update.
 //
-// Rank g of G holds rows [lo_g, hi_g) of the last spatial mode s = d-2 of
-// every slice, so its slab is a contiguous chunk of the colexicographic
-// slice. Modes 0..s-1 are projected locally; the one per-slice exchange is
+// Rank g of G holds rows [lo_g, hi_g) of one spatial mode s of every slice
+// (a dense sub-tensor; a contiguous chunk of the colexicographic slice when
+// s is the last spatial mode). Modes 0..s-1 are projected locally; the one per-slice exchange is
 // an allgather of [partial norm pairs | compressed local tensor] (the input
 // of mode s restricted to the rank's rows). Every rank then assembles the
 // identical full compressed tensor and partial pairs from the identical
@@ -32,7 +32,7 @@ __global__ void shard_pack_pairs_kernel(ShardPairs p, double* out) {
   }
 }
 
-// Concatenate the ranks' chunks along the last axis and regroup the partial
+// Concatenate the ranks' parts along the shard mode and regroup the partial
 // pairs per mode: pairs_out[k * 2G + 2g + j] = recv[g * count + 2k + j].
 __global__ void shard_unpack_kernel(ShardLayout L, const double* __restrict__ recv,
                                     double* __restrict__ z, double* __restrict__ pairs_out) {
@@ -43,12 +43,16 @@ __global__ void shard_unpack_kernel(ShardLayout L, const double* __restrict__ re
       const int k = i >> 1, j = i & 1;
       pairs_out[(long long)k * 2 * L.world + 2 * g + j] = src[i];
     }
-  const long long n = L.inner * L.nloc[g];
+  const long long chunk = L.inner * L.nloc[g];  // contiguous run per outer index
+  const long long n = chunk * L.outer;
   double* dst = z + L.inner * L.lo[g];
+  const long long pitch = L.inner * L.ns;
   src += L.header;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x)
-    dst[i] = src[i];
+       i += (long long)gridDim.x * blockDim.x) {
+    const long long o = i / chunk;
+    dst[(i - o * chunk) + o * pitch] = src[i];
+  }
 }
 
 }  // namespace
@@ -61,7 +65,10 @@ void launch_shard_pack_pairs(const ShardPairs& p, double* out, cudaStream_t st) 
 void launch_shard_unpack(const ShardLayout& L, const double* recv, double* z, double* pairs_out,
                          cudaStream_t st) {
   long long mx = 1;
-  for (int g = 0; g < L.world; ++g) mx = L.inner * L.nloc[g] > mx ? L.inner * L.nloc[g] : mx;
+  for (int g = 0; g < L.world; ++g) {
+    const long long e = L.inner * L.nloc[g] * L.outer;
+    mx = e > mx ? e : mx;
+  }
   long long bx = (mx + 255) / 256;
   if (bx > 2 * kNumSMs) bx = 2 * kNumSMs;
   if (bx < 1) bx = 1;

@@ -2,9 +2,10 @@
 
 The reference has no distributed mode; its ``stream_update``
 (streaming.hpp:63, streaming.cpp:157-233) is a sequential chain over the
-non-streaming modes. Sharding one slice along its LAST spatial mode
-``s = d-2`` keeps every rank's slab contiguous and makes the one exchange the
-compressed tensor:
+non-streaming modes. Each slice is sharded along ONE spatial mode ``s`` — by
+default the largest (the last one on ties, so the slab is a contiguous chunk
+and the exchange the smallest), or the one the caller names (BASELINE
+configs[2]: mode 1):
 
 * rank g holds rows ``[bounds[g], bounds[g+1])`` of mode s of every slice and
   projects modes ``0 .. s-1`` of its slab locally (``tsg_shard_begin``);
@@ -16,8 +17,12 @@ compressed tensor:
   gathered bytes and runs mode s onward, the decision and the insertion
   redundantly (``tsg_shard_continue``). All reductions over ranks run in rank
   order on those bytes, so all ranks stay bitwise identical and no factor is
-  ever broadcast. Basis growth at a local mode (rare) requests one more
-  allgather of that mode's input and grows redundantly.
+  ever broadcast;
+* basis growth at a local mode k < s: every rank forms the N_k x N_k Gram of
+  its part of the residual, ONE all-reduce sums them (N_k^2 doubles), the
+  eigensolve runs redundantly, ``K = W^T E`` and the remaining local modes
+  stay local, and the slice continues with a fresh compressed-tensor gather
+  (sthosvd.cpp:45-59, streaming.cpp:142-151 split over the ranks).
 
 ``ShardedStreamingState`` drives the protocol over any ``comm`` with an
 ``allgather(send, recv)`` method; ``TorchComm`` wraps torch.distributed
@@ -46,12 +51,33 @@ def shard_bounds(n: int, world: int) -> list[int]:
     return b
 
 
-def slab_of(slice_flat, slice_dims, bounds, rank):
+def default_shard_mode(slice_dims) -> int:
+    """The largest spatial mode, the last one on ties (tsg_shard_setup)."""
+    m = 0
+    for k, n in enumerate(slice_dims):
+        if n >= slice_dims[m]:
+            m = k
+    return m
+
+
+def slab_of(slice_flat, slice_dims, bounds, rank, mode=None):
     """Rank `rank`'s slab of a flat colexicographic slice: rows
-    [bounds[rank], bounds[rank+1]) of the last spatial mode (a contiguous
-    chunk; works for numpy arrays and torch tensors alike)."""
-    inner = int(np.prod(slice_dims[:-1]))
-    return slice_flat[bounds[rank] * inner: bounds[rank + 1] * inner]
+    [bounds[rank], bounds[rank+1]) of spatial mode `mode` (default: the
+    default shard mode) as a flat colexicographic dense tensor. A contiguous
+    view when `mode` is the last spatial mode, a copy otherwise; works for
+    numpy arrays and torch tensors alike."""
+    nd = len(slice_dims)
+    if mode is None:
+        mode = default_shard_mode(slice_dims)
+    lo, hi = bounds[rank], bounds[rank + 1]
+    if mode == nd - 1:
+        inner = int(np.prod(slice_dims[:-1]))
+        return slice_flat[lo * inner: hi * inner]
+    t = slice_flat.reshape(tuple(slice_dims)[::-1])  # row-major view of the colex tensor
+    ax = nd - 1 - mode
+    if isinstance(slice_flat, np.ndarray):
+        return np.ascontiguousarray(np.take(t, np.arange(lo, hi), axis=ax)).reshape(-1)
+    return t.narrow(ax, lo, hi - lo).contiguous().reshape(-1)
 
 
 def device_view(ptr: int, n: int, device: int):
@@ -84,6 +110,19 @@ class TorchComm:
         else:
             self.dist.all_gather(outs, send, group=self.group)
 
+    def allreduce(self, send, recv, stream=None) -> None:
+        """recv = sum over ranks of send — the same bytes on every rank (NCCL
+        and gloo all-reduce both distribute one reduced value per element)."""
+        def run():
+            recv.copy_(send)
+            self.dist.all_reduce(recv, op=self.dist.ReduceOp.SUM, group=self.group)
+        if stream is not None:
+            import torch
+            with torch.cuda.stream(stream):
+                run()
+        else:
+            run()
+
 
 class ShardedStreamingState(S.StreamingState):
     """A StreamingState whose updates are split over G ranks (tsg_shard_*).
@@ -100,12 +139,18 @@ class ShardedStreamingState(S.StreamingState):
         self.exchanges = 0
         self.exchanged_doubles = 0
 
-    def setup(self, rank: int, world: int, bounds=None):
+    def setup(self, rank: int, world: int, bounds=None, mode=None):
+        """Split mode `mode` (default: the largest spatial mode, the last one on
+        ties) over `world` ranks; `bounds` defaults to an even split."""
+        dims = self.query()["slice_dims"]
+        if mode is None:
+            mode = default_shard_mode(dims)
         if bounds is None:
-            bounds = shard_bounds(self.query()["slice_dims"][-1], world)
+            bounds = shard_bounds(dims[mode], world)
         b = np.asarray(bounds, dtype=np.int64)
-        self._check(self.L.tsg_shard_setup(self.h, rank, world, b.ctypes.data_as(S._i64p)))
-        self.rank, self.world, self.bounds = rank, world, [int(v) for v in b]
+        self._check(self.L.tsg_shard_setup_mode(self.h, rank, world, mode, b.ctypes.data_as(S._i64p)))
+        self.rank, self.world, self.bounds, self.mode = rank, world, [int(v) for v in b], mode
+        self.exchange_log = []  # (op, doubles per rank) of every exchange
         return self.bounds
 
     # -- protocol steps (also used by LoopbackGroup) --
@@ -120,8 +165,18 @@ class ShardedStreamingState(S.StreamingState):
         return ex
 
     def exchange_tensors(self, ex: S.TsgExchange):
+        nrecv = ex.count if ex.op == S.XCHG_ALLREDUCE_SUM else ex.count * self.world
+        if hasattr(self, "exchange_log"):
+            self.exchange_log.append((int(ex.op), int(ex.count)))
         return (device_view(ex.send, ex.count, self.device),
-                device_view(ex.recv, ex.count * self.world, self.device))
+                device_view(ex.recv, nrecv, self.device))
+
+    def sync_exchange(self) -> None:
+        """Drain the engine's stream and the device's current torch stream: used
+        by drive() around a collective that is not ordered on the engine's stream."""
+        import torch
+        torch.cuda.ExternalStream(self.cuda_stream(), device=self.device).synchronize()
+        torch.cuda.current_stream(self.device).synchronize()
 
     def stream_update_slab(self, slab, comm) -> None:
         """One sharded stream_update: local pass, allgather(s), redundant finish.
@@ -136,14 +191,28 @@ class ShardedStreamingState(S.StreamingState):
 def drive(engine, slab, comm, stream=None) -> tuple[int, int]:
     """The per-slice protocol of include/tsg.h over any engine exposing
     begin / exchange_tensors / cont and any comm exposing allgather.
-    Returns (exchanges, doubles gathered per rank x world)."""
+    Returns (exchanges, doubles gathered per rank x world).
+
+    tsg_shard_begin / tsg_shard_continue return as soon as the local pass is
+    ENQUEUED on the engine's stream, so the send buffer is only valid in that
+    stream's order. With ``stream`` (the engine's stream) the collective is
+    ordered behind it; without one (a host-staging comm: gloo, MPI) the
+    engine's stream is drained before every exchange and the collective is
+    complete before the engine continues."""
     ex = engine.begin(slab)
     n = dbl = 0
     while ex.pending:
         send, recv = engine.exchange_tensors(ex)
-        comm.allgather(send, recv, stream=stream)
+        if stream is None:
+            engine.sync_exchange()
+        if getattr(ex, "op", S.XCHG_ALLGATHER) == S.XCHG_ALLREDUCE_SUM:
+            comm.allreduce(send, recv, stream=stream)
+        else:
+            comm.allgather(send, recv, stream=stream)
+        if stream is None:
+            engine.sync_exchange()
         n += 1
-        dbl += int(ex.count) * engine.world
+        dbl += int(ex.count) * (1 if getattr(ex, "op", 0) == S.XCHG_ALLREDUCE_SUM else engine.world)
         ex = engine.cont(ex)
     return n, dbl
 
@@ -164,13 +233,21 @@ class LoopbackGroup:
             pend = [bool(e.pending) for e in exs]
             if not any(pend):
                 return
-            if not all(pend) or len({int(e.count) for e in exs}) != 1:
-                raise RuntimeError(f"ranks diverged: pending {pend}, counts {[e.count for e in exs]}")
+            if not all(pend) or len({(int(e.count), int(e.op)) for e in exs}) != 1:
+                raise RuntimeError(f"ranks diverged: pending {pend}, "
+                                   f"requests {[(e.count, e.op) for e in exs]}")
             torch.cuda.synchronize()  # the local passes run on the engines' streams
             views = [st.exchange_tensors(e) for st, e in zip(self.states, exs)]
             cnt = int(exs[0].count)
-            for _, recv in views:
-                for g, (send, _) in enumerate(views):
-                    recv[g * cnt:(g + 1) * cnt].copy_(send)
+            if int(exs[0].op) == S.XCHG_ALLREDUCE_SUM:
+                total = views[0][0].clone()
+                for send, _ in views[1:]:   # rank order: one sum, the same bytes to every rank
+                    total += send
+                for _, recv in views:
+                    recv.copy_(total)
+            else:
+                for _, recv in views:
+                    for g, (send, _) in enumerate(views):
+                        recv[g * cnt:(g + 1) * cnt].copy_(send)
             torch.cuda.synchronize()
             exs = [st.cont(e) for st, e in zip(self.states, exs)]

@@ -84,9 +84,13 @@ class TsgDims(C.Structure):
 
 
 class TsgExchange(C.Structure):
-    """tsg_exchange (include/tsg.h): one allgather request of a sharded update."""
-    _fields_ = [("pending", C.c_int32), ("count", C.c_int64), ("send", C.c_void_p),
-                ("recv", C.c_void_p)]
+    """tsg_exchange (include/tsg.h): one collective request of a sharded update
+    (op 0: allgather, op 1: all-reduce sum)."""
+    _fields_ = [("pending", C.c_int32), ("op", C.c_int32), ("count", C.c_int64),
+                ("send", C.c_void_p), ("recv", C.c_void_p)]
+
+
+XCHG_ALLGATHER, XCHG_ALLREDUCE_SUM = 0, 1
 
 
 class TsgMetrics(C.Structure):
@@ -106,7 +110,7 @@ EXPORTED = [
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
     "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
-    "tsg_shard_setup", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
+    "tsg_shard_setup", "tsg_shard_setup_mode", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
     "tsg_error_sums", "tsg_profile_timeline", "tsg_save_checkpoint", "tsg_load_checkpoint",
 ]
 
@@ -160,6 +164,7 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.tsg_readback_bytes_per_update.argtypes = []
     L.tsg_readback_bytes_per_update.restype = C.c_int64
     L.tsg_shard_setup.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _i64p]
+    L.tsg_shard_setup_mode.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _i64p]
     L.tsg_shard_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TsgExchange)]
     L.tsg_shard_continue.argtypes = [C.c_void_p, C.POINTER(TsgExchange)]
     L.tsg_profile_timeline.argtypes = [C.c_void_p, _dp, C.c_int64]

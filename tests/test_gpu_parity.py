@@ -411,7 +411,8 @@ def test_mode_subspace_gram_vs_numpy(dims, mode):
     assert disc == pytest.approx(w[r:].sum(), rel=1e-10, abs=1e-12 * w[0])
 
 
-@pytest.mark.parametrize("dims", [(16, 40, 300), (5, 7, 900), (32, 64, 50), (33, 20, 80)])
+@pytest.mark.parametrize("dims", [(16, 40, 300), (5, 7, 900), (32, 64, 50), (33, 20, 80),
+                                  (48, 100, 50)])
 def test_mode_subspace_gram_narrow_modes(dims):
     """Narrow modes (rows <= 32: the Gram's K steps are split over the warps
     and summed in a fixed order) and the first size past it, against numpy."""

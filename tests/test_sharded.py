@@ -50,6 +50,24 @@ def test_shard_bounds_and_slabs():
                                   t[:, :, b[1]:b[2]])
 
 
+def test_slab_of_any_mode_and_default_mode():
+    from paper_2308_16395_b200 import sharded as SH
+    assert SH.default_shard_mode((200, 200, 200)) == 2       # ties: the last one
+    assert SH.default_shard_mode((384, 384, 384, 16)) == 2   # C4: not the variable mode
+    assert SH.default_shard_mode((12, 10, 9)) == 0
+    dims = (4, 5, 6)
+    y = np.arange(np.prod(dims), dtype=np.float64)
+    t = y.reshape(dims[::-1]).transpose()  # t[i0, i1, i2]
+    for mode in range(3):
+        b = SH.shard_bounds(dims[mode], 2)
+        for g in range(2):
+            want = np.take(t, np.arange(b[g], b[g + 1]), axis=mode)
+            got = SH.slab_of(y, dims, b, g, mode=mode)
+            np.testing.assert_array_equal(got, want.transpose().ravel())  # colexicographic
+            tt = SH.slab_of(torch.from_numpy(y), dims, b, g, mode=mode)
+            np.testing.assert_array_equal(tt.numpy(), got)
+
+
 def test_local_projection_then_gather_equals_full():
     """Modes < s are local to a slab of the last spatial mode: project each
     slab, concatenate along s == project the slice (streaming.cpp:126-133)."""
@@ -80,6 +98,8 @@ class _HostEngine:
     runs the CPU checker on the gathered slice."""
 
     class Ex:
+        op = 0  # allgather
+
         def __init__(self, pending, count):
             self.pending, self.count = pending, count
 
@@ -98,6 +118,9 @@ class _HostEngine:
 
     def exchange_tensors(self, ex):
         return self.send, self.recv
+
+    def sync_exchange(self):
+        self.syncs = getattr(self, "syncs", 0) + 1
 
     def cont(self, ex):
         r = self.recv.numpy().reshape(self.world, self.count)
@@ -131,7 +154,7 @@ def _gloo_worker(rank, world, port, out_dir):
     ex_total = 0
     for t in range(cfg.n_init, cfg.n_slices):
         y = gen.slice_numpy(t)
-        n, _ = SH.drive(eng, SH.slab_of(y, dims, bounds, rank), comm)
+        n, _ = SH.drive(eng, SH.slab_of(y, dims, bounds, rank, mode=len(dims) - 1), comm)
         ex_total += n
     st = h.export()
     rec = {"rank": rank, "exchanges": ex_total, "core": [float(v) for v in np.ravel(st.core)],
@@ -166,19 +189,32 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def _run_loopback(case, world, bounds=None):
+def _run_loopback(case, world, bounds=None, mode=None):
     from paper_2308_16395_b200 import sharded as SH
     states = []
     for g in range(world):
         st = SH.ShardedStreamingState(device=0)
         st.init_flat(case.init_flat, case.init_dims, case.tau)
-        b = st.setup(g, world, bounds)
+        b = st.setup(g, world, bounds, mode)
         states.append(st)
     grp = SH.LoopbackGroup(states)
     dims = tuple(case.init_dims[:-1])
     for y in case.slices:
-        grp.stream_update([np.ascontiguousarray(SH.slab_of(y, dims, b, g)) for g in range(world)])
+        grp.stream_update([np.ascontiguousarray(SH.slab_of(y, dims, b, g, states[0].mode))
+                           for g in range(world)])
     return states
+
+
+def _assert_ranks_identical(ex):
+    for other in ex[1:]:
+        assert other.core_dims == ex[0].core_dims
+        np.testing.assert_array_equal(other.core, ex[0].core)
+        np.testing.assert_array_equal(other.left, ex[0].left)
+        np.testing.assert_array_equal(other.sigma, ex[0].sigma)
+        for a, b in zip(other.factors, ex[0].factors):
+            np.testing.assert_array_equal(a, b)
+        assert other.squared_error == ex[0].squared_error
+        assert other.nonstream_discarded_sq == ex[0].nonstream_discarded_sq
 
 
 @pytest.mark.gpu
@@ -192,20 +228,83 @@ def test_loopback_sharded_vs_golden(golden, name, world):
         pytest.skip("fewer rows than ranks")
     states = _run_loopback(case, world)
     ex = [st.export() for st in states]
-    for other in ex[1:]:  # every rank bitwise identical
-        assert other.core_dims == ex[0].core_dims
-        np.testing.assert_array_equal(other.core, ex[0].core)
-        np.testing.assert_array_equal(other.left, ex[0].left)
-        np.testing.assert_array_equal(other.sigma, ex[0].sigma)
-        for a, b in zip(other.factors, ex[0].factors):
-            np.testing.assert_array_equal(a, b)
-        assert other.squared_error == ex[0].squared_error
-        assert other.nonstream_discarded_sq == ex[0].nonstream_discarded_sq
+    _assert_ranks_identical(ex)  # every rank bitwise identical
     g = golden("stream_" + name)
     mg = P.metrics_arrays(states[0].metrics(), ex[0].order)
     mc = P.compare_metrics(mg, P.golden_metrics(g), float(g["total_input_sq"]))
     sc = P.compare_states(ex[0], P.state_from_golden(g))
     print(name, world, mc, sc)
+    P.assert_parity(mc, sc)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name,world,mode", [("c3_40", 2, 0), ("c3_40", 3, 1), ("growth24", 2, 0),
+                                             ("growth24", 3, 1), ("order5", 2, 1), ("order5", 2, 2),
+                                             ("edges", 2, 0), ("random_full", 2, 1)])
+def test_loopback_selectable_shard_mode_vs_golden(golden, name, world, mode):
+    """tsg_shard_setup_mode: the slice split along a named spatial mode (BASELINE
+    configs[2] shards along mode 1): modes before it are local, the rest runs
+    redundantly on the gathered tensor. Ranks bitwise identical, golden parity."""
+    _need_gpu()
+    case = cases.STREAM_CASES[name]()
+    if mode > len(case.init_dims) - 2 or case.init_dims[mode] < world:
+        pytest.skip("mode not available")
+    states = _run_loopback(case, world, mode=mode)
+    ex = [st.export() for st in states]
+    _assert_ranks_identical(ex)
+    g = golden("stream_" + name)
+    mc = P.compare_metrics(P.metrics_arrays(states[0].metrics(), ex[0].order), P.golden_metrics(g),
+                           float(g["total_input_sq"]))
+    sc = P.compare_states(ex[0], P.state_from_golden(g))
+    print(name, world, mode, mc, sc)
+    P.assert_parity(mc, sc)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world,mode", [(2, None), (4, None), (3, 1)])
+def test_local_mode_growth_exchanges_partial_gram(oracle, world, mode):
+    """Basis growth at a LOCAL mode (sthosvd.cpp:45-59 and
+    streaming.cpp:142-151 split over the ranks): the ranks all-reduce the
+    N_k x N_k partial Gram of their residual parts, solve redundantly and keep
+    K = W^T E local — the mode's input is never gathered. Asserts, per
+    exchange, doubles per rank <= max(N_k^2, compressed tensor + pairs), that
+    the all-reduces carry exactly N_k^2 doubles, ranks bitwise identical and
+    parity with the CPU checker."""
+    _need_gpu()
+    from paper_2308_16395_b200 import datagen as dg, streaming as S
+    cfg = dg.scaled(dg.CONFIGS["c5"], (40, 36, 44), n_slices=30, n_init=6, name="c5_local_growth")
+    cfg.growth = (3, 2, 8, 9)   # spatial ranks 3 -> 9, +2 every 8 slices
+    cfg.spatial_ranks = (9, 9, 9)
+    cfg.time_rank = 9
+    case = cases.config_case(cfg)
+    states = _run_loopback(case, world, mode=mode)
+    ex = [st.export() for st in states]
+    _assert_ranks_identical(ex)
+    smode = states[0].mode
+    dims = tuple(case.init_dims[:-1])
+    log = states[0].exchange_log
+    reduces = [c for op, c in log if op == S.XCHG_ALLREDUCE_SUM]
+    gathers = [c for op, c in log if op == S.XCHG_ALLGATHER]
+    assert reduces, "the stream never grew a local mode"
+    local_sq = {(dims[k] * dims[k] + 1) // 2 * 2 for k in range(smode)}
+    assert set(reduces) <= local_sq, (reduces, local_sq)
+    # every gather is a compressed tensor: ranks of the local modes x the
+    # rank's rows x the uncompressed modes after the shard mode (+ pairs)
+    ranks = ex[0].core_dims
+    rows = max(b - a for a, b in zip(states[0].bounds[:-1], states[0].bounds[1:]))
+    comp = int(np.prod(ranks[:smode])) * rows * int(np.prod(dims[smode + 1:])) + 2 * smode + 2
+    assert max(gathers) <= comp, (max(gathers), comp)
+    masks = [m["expanded_mask"] for m in states[0].metrics()]
+    assert any(m & ((1 << smode) - 1) for m in masks)
+    x = case.init_flat.reshape(case.init_dims[::-1]).transpose()
+    ho = oracle.stream_init(x, case.tau)
+    for y in case.slices:
+        ho.update_flat(y)
+    so = ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(states[0].metrics(), ex[0].order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(ex[0], so)
+    print("local growth", world, smode, "exchanges", len(log), "allreduces", len(reduces), mc, sc)
     P.assert_parity(mc, sc)
 
 
@@ -233,6 +332,43 @@ def test_sharded_uneven_bounds_and_errors(golden):
     st.setup(0, 2)
     with pytest.raises(S.InvalidArgument):
         st.cont(S.TsgExchange())            # nothing pending
+
+
+class _SideStreamComm:
+    """World-1 comm whose copy runs on its own NON-blocking torch stream: not
+    ordered behind the engine's stream unless drive() synchronises."""
+
+    def __init__(self):
+        self.side = torch.cuda.Stream()
+
+    def allgather(self, send, recv, stream=None):
+        assert stream is None
+        with torch.cuda.stream(self.side):
+            recv.copy_(send, non_blocking=True)
+
+    allreduce = allgather
+
+
+@pytest.mark.gpu
+def test_drive_without_stream_orders_exchange():
+    """drive(stream=None) over libtsg: the exchange buffers are
+    only valid in the engine stream's order, so drive() must drain that stream
+    around a collective issued elsewhere. Same bytes as the loopback path."""
+    _need_gpu()
+    from paper_2308_16395_b200 import sharded as SH
+    case = cases.STREAM_CASES["growth24"]()
+    st = SH.ShardedStreamingState(device=0)
+    st.init_flat(case.init_flat, case.init_dims, case.tau)
+    b = st.setup(0, 1)
+    comm = _SideStreamComm()
+    dims = tuple(case.init_dims[:-1])
+    for y in case.slices:
+        SH.drive(st, np.ascontiguousarray(SH.slab_of(y, dims, b, 0)), comm)
+    e = st.export()
+    ref = _run_loopback(case, 1)[0].export()
+    np.testing.assert_array_equal(e.core, ref.core)
+    np.testing.assert_array_equal(e.left, ref.left)
+    np.testing.assert_array_equal(e.sigma, ref.sigma)
 
 
 def _nccl_worker(rank, world, port, q):
