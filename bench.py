@@ -208,6 +208,21 @@ def base_config(args, cfg, parallelism):
             "slice_source": slice_source(cfg), "parallelism": parallelism}
 
 
+def spin_up(dev, seconds: float = 0.4):
+    """Bring the GPU out of its idle power state before the warm-up: the
+    slices are synthesised on the host (tens of seconds with an idle GPU) and
+    W warm-up updates last well under a millisecond, too short for the clocks
+    to ramp. Dense fp32 products for `seconds`; they also flush L2."""
+    import torch
+    a = torch.randn(4096, 4096, device=dev)
+    torch.cuda.synchronize(dev)
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(8):
+            a = (a @ a).clamp_(-1.0, 1.0)
+        torch.cuda.synchronize(dev)
+
+
 # ----------------------------------------------------------------- our arm
 def init_batch(gen, cfg, dev):
     """The n_init-slice batch on the device, filled slice by slice (no
@@ -272,6 +287,7 @@ def run_ours(args, world, rank, local):
     slices = [bench_slice(gen, cfg, first + i, dev) for i in range(nsl)]
     torch.cuda.synchronize()
     ext = torch.cuda.ExternalStream(st.cuda_stream(), device=dev)
+    spin_up(dev)
     for i in range(args.warmup):
         st.stream_update(slices[i])
     st.synchronize()
@@ -312,6 +328,7 @@ def run_ours(args, world, rank, local):
         for i in range(prime):
             sp.stream_update(bench_slice(gen, cfg, cfg.n_init + i, dev))
             sp.synchronize()
+        spin_up(dev)
         for i in range(args.warmup):
             sp.stream_update(slices[i])
         sp.synchronize()
@@ -455,13 +472,14 @@ def run_sharded(args, world, rank, local):
     st = SH.ShardedStreamingState(device=local)
     st.init_flat(init, gen.init_dims(), cfg.tau)
     del init
-    bounds = st.setup(rank, world)
+    bounds = st.setup(rank, world, mode=args.shard_mode)
     dims = cfg.slice_dims
     nsl = args.warmup + args.steps
-    slabs = [SH.slab_of(bench_slice(gen, cfg, cfg.n_init + i, dev), dims, bounds, rank).clone()
+    slabs = [SH.slab_of(bench_slice(gen, cfg, cfg.n_init + i, dev), dims, bounds, rank, st.mode).clone()
              for i in range(nsl)]
     torch.cuda.synchronize()
     comm = SH.TorchComm() if world > 1 else _LocalComm()
+    spin_up(dev)
     for i in range(args.warmup):
         st.stream_update_slab(slabs[i], comm)
     launches0 = st.kernel_launches()
@@ -483,6 +501,38 @@ def run_sharded(args, world, rank, local):
     ms = allreduce_max(world, e0.elapsed_time(e1))
     q = st.query()
     value = args.steps / (ms / 1e3)
+    # roofline of the dominant kernel work: the LOCAL projection pass of the
+    # slab (modes before the shard mode), event-timed on the engine's stream
+    # over a few extra updates (begin = local pass enqueued; the events
+    # bracket it before the exchange is issued)
+    local_ms, n_local = 0.0, min(8, args.steps)
+    for i in range(n_local):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(ext)
+        ex = st.begin(slabs[args.warmup + i])
+        a1.record(ext)
+        while ex.pending:
+            send, recv = st.exchange_tensors(ex)
+            (comm.allreduce if ex.op == 1 else comm.allgather)(send, recv, stream=ext)
+            ex = st.cont(ex)
+        a1.synchronize()
+        local_ms += a0.elapsed_time(a1)
+    local_ms = allreduce_max(world, local_ms / max(n_local, 1))
+    ranks_now = list(st.query()["core_dims"])
+    slab_elems = int(slabs[0].numel())
+    smode = st.mode
+    lbytes = 8.0 * slab_elems * (1.0 + (ranks_now[0] / dims[0] if smode > 0 else 0.0))
+    hbm, hbm_kind = load_peaks()
+    roof = {"bound": "hbm", "achieved": lbytes / (local_ms / 1e3) / 1e9 if smode > 0 else None,
+            "peak": hbm, "unit": "GB/s",
+            "frac": (lbytes / (local_ms / 1e3) / 1e9 / hbm) if smode > 0 else None,
+            "kernel": "local projection pass of the rank's slab (modes < shard mode; mode 0 dominates)",
+            "algorithmic_bytes_per_launch": lbytes, "avg_launch_ms": local_ms,
+            "peak_source": f"{hbm_kind} MEASURED_PEAKS.json hbm_gbs", "traffic": None,
+            "timing": f"CUDA events around tsg_shard_begin's local pass, {n_local} extra updates, max over ranks"}
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_from_state(args, cfg, st, slabs)
     # end to end: pinned host slabs through the public sharded API (H2D inside)
     e2e = None
     if args.e2e_steps > 0:
@@ -509,16 +559,14 @@ def run_sharded(args, world, rank, local):
         "gbs_ingested": value * cfg.slice_bytes / 1e9,
         "config": base_config(args, cfg, f"sharded{world}"),
         "run": {"ranks_after": list(q["core_dims"]), "n_d_after": q["n_d"],
-                "shard_rows": list(bounds),
+                "shard_mode": st.mode, "shard_rows": list(bounds),
                 "l2": "each step reads a distinct device-resident slab (never re-read)",
                 "mode": "sharded engine: local modes, one allgather per slice, redundant finish"},
         "exchange": {"allgathers_per_step": (st.exchanges - ex0) / args.steps,
                      "bytes_gathered_per_rank_per_step":
                          8.0 * (st.exchanged_doubles - xd0) / args.steps / world},
         "clocks": clk, "gpu_launches": st.kernel_launches() - launches0,
-        "e2e": e2e, "cpu_baseline": None,
-        "roofline": {"bound": "hbm", "achieved": None, "peak": load_peaks()[0], "unit": "GB/s",
-                     "frac": None, "note": "sharded mode: per-kernel timing is reported by the single-GPU engine line"},
+        "e2e": e2e, "cpu_baseline": cpu, "roofline": roof,
     }
     st.close()
     return out
@@ -661,6 +709,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--cpu-slices", type=int, default=40)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard-mode", type=int, default=None,
+                    help="spatial mode split over the GPUs (default: the largest, the last one on ties)")
     ap.add_argument("--mode", default="auto", choices=["auto", "sharded", "replicas", "single"],
                     help="N>1: sharded (one stream split over the GPUs, default) or replicas "
                          "(independent streams); N=1: single engine (default) or sharded")

@@ -648,10 +648,39 @@ struct tsg_stream {
       s.owned.push_back(reinterpret_cast<double*>(rk_d));
     }
     double* disc_d = reinterpret_cast<double*>(rk_d) + 1;
+    double* ev = dalloc(rows);
+    s.owned.push_back(ev);
+    if (tri_eig_applicable((int)rows)) {
+      // n >= 96: tridiagonal route — all eigenvalues for the truncation rule,
+      // then only the retained eigenvectors (tridiag_eig.cu)
+      const int max_rank = tri_eig_max_rank((int)rows);
+      double* twork = dalloc(tri_eig_work_doubles((int)rows, max_rank));
+      s.owned.push_back(twork);
+      if (launch_tri_eigvals(g, (int)rows, ev, twork, st)) {
+        launch_truncate(ev, (int)rows, delta, 0, rk_d, disc_d, st);
+        long long hr[2];
+        ck(cudaMemcpyAsync(hr, rk_d, 16, cudaMemcpyDeviceToHost, st), "rank D2H");
+        sync();
+        ck(cudaGetLastError(), "mode_subspace");
+        if (hr[0] <= max_rank) {
+          s.rank = hr[0];
+          std::memcpy(&s.disc, &hr[1], 8);
+          double* vec = dalloc(rows * std::max(s.rank, 1LL));
+          s.owned.push_back(vec);
+          launch_tri_eigvecs((int)rows, (int)s.rank, twork, vec, st);
+          // callers may read the basis from another stream: complete it here
+          sync();
+          ck(cudaGetLastError(), "mode_subspace eigenvectors");
+          s.basis = vec;
+          s.evals = ev;
+          return;
+        }
+      }
+      // (no cooperative launch, or most of the spectrum retained: Jacobi)
+    }
     double* work = dalloc(3 * rows * rows + 512);
     double* vec = dalloc(rows * rows);
-    double* ev = dalloc(rows);
-    s.owned.insert(s.owned.end(), {work, vec, ev});
+    s.owned.insert(s.owned.end(), {work, vec});
     launch_sym_eig(g, (int)rows, ev, vec, work, nullptr, st);
     launch_truncate(ev, (int)rows, delta, 0, rk_d, disc_d, st);
     long long hr[2];
@@ -926,7 +955,16 @@ struct tsg_stream {
     B.capr = capr;
     B.order = d;
     static const int rpad = std::getenv("TSG_RHINT_PAD") ? std::atoi(std::getenv("TSG_RHINT_PAD")) : 0;
-    B.r_hint = std::min(r_ub + rpad, capr - 1);
+    // The hint is an upper bound of the rank the kernel will find (it selects
+    // the register-bound template and the Q columns staged). On the graph
+    // path it is part of the key: the count of undrained insertions wobbles
+    // between 1 and kNP with the record ring's publication lag, which made
+    // new (slot, hint) pairs — each a 1-3 ms capture — appear long after the
+    // warm-up. The pipelined engine therefore rounds it up to the steady
+    // bound r + kNP (arithmetic is RMAX-invariant, see DESIGN).
+    int r_key = r_ub;
+    if (s_ == si && (flags & TSG_ASYNC)) r_key = std::max(r_ub, r_exact + kNP);
+    B.r_hint = std::min(r_key + rpad, capr - 1);
     B.commit_modes = commit ? d - 1 : 0;  // ledger commit fused into the insertion
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
     const bool graph = (s_ == si);

@@ -208,6 +208,13 @@ void launch_diff_sumsq(const double* x, const double* y, long long n, double* pa
 // ------------------------------------------------------ sharded update
 constexpr int kMaxShards = 64;
 // Partial pairs of the locally projected modes (layout as in DecideArgs).
+// Tridiagonal route for the leading eigenpairs of a Gram matrix (tridiag_eig.cu).
+bool tri_eig_applicable(int n);
+int tri_eig_max_rank(int n);
+long long tri_eig_work_doubles(int n, int max_rank);
+bool launch_tri_eigvals(const double* g, int n, double* evals, double* work, cudaStream_t st);
+void launch_tri_eigvecs(int n, int rank, double* work, double* evecs, cudaStream_t st);
+
 struct ShardPairs {
   const double* partial;
   int off[kMaxD], cnt[kMaxD];

@@ -48,17 +48,20 @@ struct Entry {
 // A handful of live handles (streams a program interleaves); the oldest is
 // released when the cache is full.
 constexpr std::size_t kCacheSize = 8;
-std::list<Entry>& cache() {
-  static std::list<Entry> c;
-  return c;
-}
-
-struct CacheCleanup {
-  ~CacheCleanup() {
-    for (Entry& e : cache()) tsg_destroy(e.h);
-    cache().clear();
+// The list and its clean-up are ONE function-local static: a separate
+// namespace-scope clean-up object would outlive the list (statics die in
+// reverse order of construction) and walk freed nodes at exit.
+struct Cache {
+  std::list<Entry> entries;
+  ~Cache() {
+    for (Entry& e : entries) tsg_destroy(e.h);
+    entries.clear();
   }
-} g_cleanup;
+};
+std::list<Entry>& cache() {
+  static Cache c;
+  return c.entries;
+}
 
 tsg_stream* new_handle(std::size_t reorth) {
   tsg_config cfg;

@@ -411,6 +411,59 @@ def test_mode_subspace_gram_vs_numpy(dims, mode):
     assert disc == pytest.approx(w[r:].sum(), rel=1e-10, abs=1e-12 * w[0])
 
 
+def _tensor_with_mode0_spectrum(g, n, cols, sv):
+    """n x cols matrix with prescribed singular values sv (len <= n)."""
+    u = np.linalg.qr(g.standard_normal((n, n)))[0]
+    v = np.linalg.qr(g.standard_normal((cols, n)))[0]
+    s = np.zeros(n)
+    s[: len(sv)] = sv
+    return (u * s[None, :]) @ v.T
+
+
+@pytest.mark.parametrize("n,kind", [(96, "lowrank"), (130, "decay"), (200, "cluster"), (256, "lowrank"),
+                                    (384, "decay"), (384, "cluster"), (101, "pairs"), (512, "lowrank")])
+def test_mode_subspace_tridiagonal_route_vs_numpy(n, kind):
+    """mode_subspace for n >= 96 (tridiag_eig.cu: Householder tridiagonal form,
+    Sturm multisection, inverse iteration on the retained eigenvalues, back
+    transformation) against float64 numpy: every eigenvalue to 1e-12 of the
+    largest, the retained basis orthonormal to 1e-13 and spanning numpy's
+    leading eigenspace, each retained column an eigenvector (residual
+    <= 1e-11 ||G||), the sign rule of linalg.cpp:170-178, and the discarded
+    energy. Spectra: low rank + noise floor (growth epochs), geometric decay
+    (config 3/4-like), exactly repeated retained eigenvalues (cluster
+    handling) and close pairs."""
+    g = np.random.default_rng(n * 3 + len(kind))
+    cols = n + 40
+    if kind == "lowrank":
+        sv = np.concatenate([np.linspace(10, 3, 9), 1e-5 * (1 + g.random(n - 9))])
+    elif kind == "decay":
+        sv = 0.9 ** np.arange(n)
+    elif kind == "cluster":
+        sv = np.concatenate([[5.0] * 4, [3.0] * 3, [2.0, 1.5], 1e-4 * (1 + g.random(n - 9))])
+    else:
+        sv = np.concatenate([np.repeat(np.linspace(8, 2, 6), 2) * (1 + 1e-9 * np.arange(12)),
+                             1e-4 * (1 + g.random(n - 12))])
+    a = _tensor_with_mode0_spectrum(g, n, cols, sv)
+    t = a.reshape(n, cols // 4, 4) if cols % 4 == 0 else a.reshape(n, cols, 1)
+    gram = a @ a.T
+    w, v = np.linalg.eigh(gram)
+    w, v = w[::-1], v[:, ::-1]
+    delta = np.sqrt(np.sum(w[9 if kind != "pairs" else 12:]) * 1.5) if kind != "decay" else 0.05 * np.linalg.norm(a)
+    basis, ev, disc = S.mode_subspace(t, 0, float(delta))
+    np.testing.assert_allclose(ev, np.maximum(w, 0), rtol=0, atol=1e-12 * w[0])
+    r = basis.shape[1]
+    assert 1 <= r < n
+    assert np.abs(basis.T @ basis - np.eye(r)).max() < 1e-13
+    # eigenvector residuals and the leading eigenspace
+    res = gram @ basis - basis * ev[None, :r]
+    assert np.abs(res).max() <= 1e-11 * w[0], np.abs(res).max() / w[0]
+    if w[r - 1] - w[r] > 1e-6 * w[0]:
+        assert np.abs(basis @ basis.T - v[:, :r] @ v[:, :r].T).max() < 1e-9
+    for j in range(r):  # sign rule: the entry of largest magnitude is positive
+        assert basis[np.argmax(np.abs(basis[:, j])), j] > 0
+    assert disc == pytest.approx(w[r:].clip(min=0).sum(), rel=1e-9, abs=1e-12 * w[0])
+
+
 @pytest.mark.parametrize("dims", [(16, 40, 300), (5, 7, 900), (32, 64, 50), (33, 20, 80),
                                   (48, 100, 50)])
 def test_mode_subspace_gram_narrow_modes(dims):

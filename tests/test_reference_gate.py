@@ -25,6 +25,7 @@ def test_reference_acceptance_gate_through_gpu_shim():
         pytest.skip("shim/_build/acceptance_gpu not built (needs the reference sources)")
     p = subprocess.run([GATE], capture_output=True, text=True, timeout=900)
     print(p.stdout[-4000:])
+    assert p.returncode >= 0, f"acceptance_gpu died with signal {-p.returncode}"
     res = dict((int(i), s) for s, i in re.findall(r"\[(PASS|FAIL)\] (\d)\.", p.stdout))
     assert len(res) == 8, p.stdout[-2000:]
     # 5: the CLI binary is not buildable here (TUCKER_CLI unset)
