@@ -44,8 +44,11 @@
  * slice are ordered after work queued earlier on the legacy default stream;
  * a producer on another non-blocking stream must synchronise first. In
  * the default synchronous mode a slice may be reused as soon as tsg_update
- * returns. With TSG_ASYNC, a slice (host or device) must stay unchanged
- * until the following tsg_update (or tsg_synchronize) returns.
+ * returns. With TSG_ASYNC the engine acts on a slice's decision two calls
+ * later (slices t+1 and t+2 are projected while slice t is inserted): a HOST
+ * slice must stay unchanged until the following tsg_update returns (its
+ * staging copy is then complete), a DEVICE slice until the second following
+ * tsg_update (or tsg_synchronize) returns.
  * The handle owns all device memory; one host thread drives a handle.
  */
 #ifndef TSG_H

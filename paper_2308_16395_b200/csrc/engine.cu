@@ -961,9 +961,9 @@ struct tsg_stream {
     // between 1 and kNP with the record ring's publication lag, which made
     // new (slot, hint) pairs — each a 1-3 ms capture — appear long after the
     // warm-up. The pipelined engine therefore rounds it up to the steady
-    // bound r + kNP (arithmetic is RMAX-invariant, see DESIGN).
+    // bound r + kNP + 1 (arithmetic is RMAX-invariant, see DESIGN).
     int r_key = r_ub;
-    if (s_ == si && (flags & TSG_ASYNC)) r_key = std::max(r_ub, r_exact + kNP);
+    if (s_ == si && (flags & TSG_ASYNC)) r_key = std::max(r_ub, r_exact + kNP + 1);
     B.r_hint = std::min(r_key + rpad, capr - 1);
     B.commit_modes = commit ? d - 1 : 0;  // ledger commit fused into the insertion
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
@@ -1018,8 +1018,23 @@ struct tsg_stream {
     const double* b = nullptr;  // projected tensor
     std::chrono::steady_clock::time_point t0;
   };
-  Pend prev;
-  bool have_prev = false;
+  // Slices whose projections are enqueued and whose decisions are not acted
+  // on yet, oldest first. The pipelined engine keeps kDefer of them: the host
+  // enqueues the projections of slice t+2 BEFORE it waits for the decision of
+  // slice t, so the projection stream always holds queued work (with one
+  // deferred slice the period was (decision latency + host turnaround) / 2).
+  static constexpr int kDefer = 2;
+  std::vector<Pend> deferred;
+  // Act on the oldest deferred slices until at most `keep` remain; when a slow
+  // path ran (bases may have grown), the younger ones are projected again.
+  void settle(size_t keep) {
+    while (deferred.size() > keep) {
+      Pend p = deferred.front();
+      deferred.erase(deferred.begin());
+      if (complete(p))
+        for (Pend& q : deferred) enqueue_proj(q.y, q);
+    }
+  }
   double* stage[kNP] = {};  // host-slice staging per slot
 
   // Mode projections + decision of one slice on `st` (a cached graph: the
@@ -1179,16 +1194,12 @@ struct tsg_stream {
     // enqueue this slice first, then settle the previous one: the projection
     // stream never waits on the host
     enqueue_proj(y, cur);
-    if (have_prev) {
-      have_prev = false;
-      if (complete(prev)) enqueue_proj(y, cur);  // bases grew: redo this slice
-    }
+    deferred.push_back(cur);
     if (flags & TSG_ASYNC) {
-      prev = cur;
-      have_prev = true;
+      settle(kDefer);
       drain(false);
     } else {
-      complete(cur);
+      settle(0);
       drain(true);
       if (have_last_ctrl && pending.empty()) {
         *ctrl_h = last_ctrl;  // the device block as the last insertion left it
@@ -1475,7 +1486,7 @@ struct tsg_stream {
     if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
     if (shard_world == 0) fail(TSG_EINVAL, "tsg_shard_begin: call tsg_shard_setup first");
     if (sh_phase != 0) fail(TSG_EINVAL, "tsg_shard_begin: the previous slice's exchange is pending");
-    if (have_prev || !pending.empty()) flush();  // a preceding async tsg_update
+    if (!deferred.empty() || !pending.empty()) flush();  // a preceding async tsg_update
     sh_t0 = std::chrono::steady_clock::now();
     const long long le = slice_elems / N[shard_mode] * shard_n[shard_rank];
     const bool misaligned = (reinterpret_cast<uintptr_t>(slab) & 15) != 0;
@@ -1676,10 +1687,7 @@ struct tsg_stream {
   }
 
   void flush() {
-    if (have_prev) {
-      have_prev = false;
-      complete(prev);
-    }
+    settle(0);
     sync();
     drain(true);
     pull_ctrl();
@@ -1860,7 +1868,9 @@ struct tsg_stream {
     sh_send_cap = sh_recv_cap = sh_stage_cap = 0;
     shard_world = 0;
     sh_phase = 0;
-    have_prev = false;
+    sh_loc = sh_p = sh_gpart = sh_unf = nullptr;
+    sh_loc_cap = sh_p_cap = sh_gpart_cap = sh_unf_cap = 0;
+    deferred.clear();
     partial_cap = ipart_cap = 0;
     evec_n = 0;
     metrics.clear();

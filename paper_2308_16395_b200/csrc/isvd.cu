@@ -244,9 +244,14 @@ __device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sU) {
 }
 
 // Block-wide version for m > 32 (G, V in smem when they fit, else global).
-__device__ void inner_solve_block(const InnerIO& io, double* G, double* V) {
+// `wide` (shared memory, kWideScratch doubles, may be null): for m <= 64 the
+// spectrum comes from the one-warp secular solver (secular::eig_rank_one_wide)
+// instead of block Jacobi on the explicit Gram matrix — ~15 us instead of
+// ~430 us at m = 37 (config 5's last epochs, config 3's r = 32).
+constexpr int kWideScratch = secular::ScratchWide::doubles() + 2 * secular::kWide;
+__device__ void inner_solve_block(const InnerIO& io, double* G, double* V, double* wide = nullptr) {
   __shared__ double red[32];
-  __shared__ int sh_rank;
+  __shared__ int sh_rank, sh_iters;
   struct RotL {
     double c, s, t;
     int p, q;
@@ -256,6 +261,26 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V) {
   const int r = io.r;
   const int m = io.deg ? r : r + 1;
   const int rows = r + 1;
+  const bool use_wide = wide != nullptr && m <= secular::kWide;
+  int sweep = 0;
+  if (use_wide) {
+    if (threadIdx.x < 32) {
+      const int lane = threadIdx.x;
+      secular::ScratchWide S = secular::scratch_wide(wide);
+      double* d_in = wide + secular::ScratchWide::doubles();
+      double* z_in = d_in + secular::kWide;
+      for (int i = lane; i < m; i += 32) {
+        const double sg = i < r ? io.sigma[i] : 0.0;
+        d_in[i] = sg * sg;
+        z_in[i] = i < r ? io.p[i] : io.k;
+      }
+      __syncwarp();
+      const int it = secular::eig_rank_one_wide(m, d_in, z_in, S, io.inner + L.lam, io.inner + L.W);
+      if (lane == 0) sh_iters = it;
+    }
+    __syncthreads();
+    sweep = sh_iters;
+  } else {
   double acc = 0.0;
   for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
     const int i = idx % m, j = idx / m;
@@ -270,7 +295,6 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V) {
     V[idx] = ((idx % m) == (idx / m)) ? 1.0 : 0.0;
   const double tol = kOffDiagTolFactor * sqrt(block_sum(acc, red));
   const int np = m + (m & 1), half = np / 2;
-  int sweep = 0;
   for (; sweep < kMaxSweeps; ++sweep) {
     double o2 = 0.0;
     for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
@@ -361,9 +385,11 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V) {
     }
   }
   __syncthreads();
+  }  // !use_wide
   double* lam = io.inner + L.lam;
   double* W = io.inner + L.W;
   int* perm = reinterpret_cast<int*>(io.inner + L.perm);
+  if (!use_wide) {
   for (int i = threadIdx.x; i < m; i += blockDim.x) {
     const double di = G[i + i * m];
     int rk = 0;
@@ -407,6 +433,7 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V) {
     }
   }
   __syncthreads();
+  }  // !use_wide (the secular solver returns sorted, signed eigenpairs)
   if (threadIdx.x == 0) sh_rank = inner_truncate(io, lam, m, sweep);
   __syncthreads();
   const int rank = sh_rank;
@@ -764,9 +791,83 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
 }
 
 // ============================================================ split path
-__global__ void pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left, int capr,
-                             double* pg) {
-  pgram_block(left, ctrl->n_d, capr, ctrl->r, pg);
+// p_gram for the split path: the same per-(l, j) row-ordered sums as
+// pgram_block, but the rows are staged through shared memory in tiles
+// (coalesced loads, double buffered) instead of every thread walking the
+// row-major factor with one dependent L2 round trip per row (390 us at
+// n_d = 400, r = 36; ~15 us tiled).
+constexpr int kPgTile = 32;
+__global__ void __launch_bounds__(1024) pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left,
+                                                      int capr, double* pg) {
+  extern __shared__ double tile[];  // 2 x kPgTile x r
+  const long long n_d = ctrl->n_d;
+  const int r = ctrl->r;
+  const int tid = threadIdx.x;
+  // up to two (l, j) pairs per thread (r <= 45 -> r^2 <= 2048)
+  const int npair = r * r;
+  int l0 = 0, j0 = 0, l1 = 0, j1 = 0;
+  bool a0 = false, a1 = false;
+  if (tid < npair) {
+    l0 = tid % r;
+    j0 = tid / r;
+    a0 = l0 <= j0;
+  }
+  if (tid + 1024 < npair) {
+    l1 = (tid + 1024) % r;
+    j1 = (tid + 1024) / r;
+    a1 = l1 <= j1;
+  }
+  double s0 = 0.0, s1 = 0.0;
+  const long long ntiles = (n_d + kPgTile - 1) / kPgTile;
+  auto load = [&](long long t, double* dst) {
+    const long long i0 = t * kPgTile;
+    for (int e = tid; e < kPgTile * r; e += 1024) {
+      const int ii = e / r, c = e % r;
+      dst[e] = (i0 + ii < n_d) ? left[(i0 + ii) * capr + c] : 0.0;
+    }
+  };
+  if (ntiles > 0) load(0, tile);
+  __syncthreads();
+  for (long long t = 0; t < ntiles; ++t) {
+    double* cur = tile + (t & 1) * kPgTile * r;
+    if (t + 1 < ntiles) load(t + 1, tile + ((t + 1) & 1) * kPgTile * r);
+    if (a0) {
+#pragma unroll 8
+      for (int ii = 0; ii < kPgTile; ++ii) {
+        const double w = cur[ii * r + j0];
+        if (w != 0.0) s0 += cur[ii * r + l0] * w;
+      }
+    }
+    if (a1) {
+#pragma unroll 8
+      for (int ii = 0; ii < kPgTile; ++ii) {
+        const double w = cur[ii * r + j1];
+        if (w != 0.0) s1 += cur[ii * r + l1] * w;
+      }
+    }
+    __syncthreads();
+  }
+  if (a0) {
+    pg[l0 + j0 * r] = s0;
+    pg[j0 + l0 * r] = s0;
+  }
+  if (a1) {
+    pg[l1 + j1 * r] = s1;
+    pg[j1 + l1 * r] = s1;
+  }
+  // r > 45: the remaining pairs the slow way (not reached by the configs)
+  for (int idx = tid + 2048; idx < npair; idx += 1024) {
+    const int l = idx % r, j = idx / r;
+    if (l > j) continue;
+    double s = 0.0;
+    for (long long i = 0; i < n_d; ++i) {
+      const double w = left[i * capr + j];
+      if (w == 0.0) continue;
+      s += left[i * capr + l] * w;
+    }
+    pg[l + j * r] = s;
+    pg[j + l * r] = s;
+  }
 }
 
 __global__ void __launch_bounds__(256) isvd_pass1_kernel(const Ctrl* ctrl, const double* __restrict__ q,
@@ -868,6 +969,7 @@ struct InnerArgs {
   int capr;
   double* inner;
   int use_smem;
+  int wide;  // secular solver for 32 < m <= 64 (scratch in dynamic shared memory)
 };
 
 __global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
@@ -920,7 +1022,7 @@ __global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
   } else {
     double* G = a.use_smem ? ism : a.inner + L.G;
     double* V = a.use_smem ? ism + (long long)m * m : a.inner + L.V;
-    inner_solve_block(io, G, V);
+    inner_solve_block(io, G, V, a.wide ? ism : nullptr);
   }
 }
 
@@ -1186,8 +1288,10 @@ bool try_small(const IsvdBufs& B, cudaStream_t st) {
 }
 }  // namespace
 
-// Fused single-CTA chain when n <= kFusedRows and r + 1 <= 32.
-constexpr long long kFusedRows = 12288;
+// Fused single-CTA chain when n <= kFusedRows and r + 1 <= 32. Beyond the
+// grid kernel's 4096 rows one CTA is the slower choice (config 5 at
+// n = 8000: 0.67 ms per insertion against ~0.1 ms for the split kernels).
+constexpr long long kFusedRows = 4096;
 
 void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   if (try_small(B0, st)) {
@@ -1235,7 +1339,8 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   double* part3 = part2 + (long long)nb * (capr + 1);
   double* part4 = part3 + nb;
   const InnerLayout L = inner_layout(capr);
-  pgram_kernel<<<1, 256, 0, st>>>(B.ctrl, B.left, capr, B.inner + L.pg);
+  pgram_kernel<<<1, 1024, sizeof(double) * 2 * kPgTile * capr, st>>>(B.ctrl, B.left, capr,
+                                                                     B.inner + L.pg);
   isvd_pass1_kernel<<<nb, 256, 0, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr, part1);
   isvd_pass2_kernel<<<nb, 256, sizeof(double) * capr, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr,
                                                             nb, part1, B.e, part2);
@@ -1257,6 +1362,9 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   ia.use_smem = smem <= 160 * 1024 ? 1 : 0;
   if (!ia.use_smem) smem = 0;
   smem = std::max(smem, sizeof(double) * 3 * 32 * 33);
+  static const bool no_wide = std::getenv("TSG_NO_WIDE_SECULAR") != nullptr;  // A/B: block Jacobi
+  ia.wide = no_wide ? 0 : 1;
+  if (ia.wide) smem = std::max(smem, sizeof(double) * (size_t)kWideScratch);
   ensure_smem(isvd_inner_kernel, smem);
   isvd_inner_kernel<<<1, 512, smem, st>>>(ia);
   const int gu = grid_for(n, 256, 148 * 4);

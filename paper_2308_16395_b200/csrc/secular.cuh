@@ -323,6 +323,207 @@ __device__ int eig_rank_one(int m, const double* d_in, const double* z_in, Scrat
 }
 
 
+// Wide variant: the same algorithm as eig_rank_one for 32 < m <= kWide (the
+// inner problem of streams whose rank passes 31: configs 3 and 5), one warp,
+// each lane taking coordinates / roots lane, lane + 32. Scratch comes from
+// the caller (shared memory): sQ and sW are m x PW (PW = kWide + 1), the
+// double arrays kWide entries each, the int arrays kWide entries each.
+constexpr int kWide = 64;
+constexpr int PW = kWide + 1;
+struct ScratchWide {
+  double *sQ, *sW;
+  double *dwork, *dK, *wK, *zK, *ls, *lt, *zh, *lamall;
+  int *idx, *perm, *flag, *kind;
+  __host__ __device__ static constexpr int doubles() { return 2 * kWide * PW + 8 * kWide + 2 * kWide; }
+};
+__device__ inline ScratchWide scratch_wide(double* base) {
+  ScratchWide S;
+  S.sQ = base;
+  S.sW = S.sQ + kWide * PW;
+  S.dwork = S.sW + kWide * PW;
+  S.dK = S.dwork + kWide;
+  S.wK = S.dK + kWide;
+  S.zK = S.wK + kWide;
+  S.ls = S.zK + kWide;
+  S.lt = S.ls + kWide;
+  S.zh = S.lt + kWide;
+  S.lamall = S.zh + kWide;
+  int* ib = reinterpret_cast<int*>(S.lamall + kWide);
+  S.idx = ib;
+  S.perm = ib + kWide;
+  S.flag = ib + 2 * kWide;
+  S.kind = ib + 3 * kWide;
+  return S;
+}
+
+// d_in (m, descending, >= 0), z_in (m): eigenvalues of diag(d) + z z^T into
+// lam (descending, clamped >= 0), eigenvectors into W (m x m column-major,
+// ld m) with the reference's sign rule. Called by one full warp.
+__device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const double* z_in, ScratchWide S,
+                                 double* lam, double* W) {
+  const int lane = threadIdx.x & 31;
+  __shared__ int sh_K, sh_rot;
+  __shared__ double sh_wsum;
+  for (int i = lane; i < m * m; i += 32) {
+    const int a = i % m, b = i / m;
+    S.sQ[a * PW + b] = (a == b) ? 1.0 : 0.0;
+  }
+  for (int i = lane; i < m; i += 32) {
+    S.dwork[i] = d_in[i];
+    S.zK[i] = z_in[i];
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double zn2 = 0.0;
+    for (int i = 0; i < m; ++i) zn2 += S.zK[i] * S.zK[i];
+    const double zn = sqrt(zn2);
+    const double tol = 8.0 * DBL_EPSILON * (S.dwork[0] + zn2);
+    for (int i = 0; i < m; ++i) S.flag[i] = (fabs(S.zK[i]) * zn <= tol) ? 1 : 0;
+    int prev = -1, rotated = 0;
+    for (int i = 0; i < m; ++i) {
+      if (S.flag[i]) continue;
+      if (prev >= 0 && fabs(S.dwork[prev] - S.dwork[i]) * fabs(S.zK[prev] * S.zK[i]) <=
+                           tol * (S.zK[prev] * S.zK[prev] + S.zK[i] * S.zK[i])) {
+        const double zp = S.zK[prev], zi = S.zK[i];
+        const double rr = hypot(zp, zi);
+        const double c = zp / rr, sn = zi / rr;
+        rotated = 1;
+        const double dp = S.dwork[prev], di = S.dwork[i];
+        S.dwork[prev] = c * c * dp + sn * sn * di;
+        S.dwork[i] = sn * sn * dp + c * c * di;
+        S.zK[prev] = rr;
+        S.zK[i] = 0.0;
+        for (int a = 0; a < m; ++a) {
+          const double qp = S.sQ[a * PW + prev], qi = S.sQ[a * PW + i];
+          S.sQ[a * PW + prev] = c * qp + sn * qi;
+          S.sQ[a * PW + i] = -sn * qp + c * qi;
+        }
+        S.flag[i] = 1;
+        continue;
+      }
+      prev = i;
+    }
+    int K = 0;
+    double wsum = 0.0;
+    for (int i = 0; i < m; ++i)
+      if (!S.flag[i]) {
+        S.idx[K] = i;
+        S.dK[K] = S.dwork[i];
+        S.wK[K] = S.zK[i] * S.zK[i];
+        wsum += S.wK[K];
+        ++K;
+      }
+    sh_K = K;
+    sh_wsum = wsum;
+    sh_rot = rotated;
+  }
+  __syncwarp();
+  const int K = sh_K;
+  int iters = 0;
+  for (int j = lane; j < K; j += 32) {
+    int o;
+    double tau;
+    iters = max(iters, solve_root(S.dK, S.wK, K, sh_wsum, j, o, tau));
+    S.ls[j] = S.dK[o];
+    S.lt[j] = tau;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) iters = max(iters, __shfl_xor_sync(FULL, iters, off));
+  __syncwarp();
+  // Loewner z-hat
+  for (int i = lane; i < K; i += 32) {
+    const double di = S.dK[i];
+    double prod = (S.ls[i] - di) + S.lt[i];
+    for (int j = 0; j < K; ++j) {
+      if (j == i) continue;
+      const double num = (S.ls[j] - di) + S.lt[j];
+      prod *= num * rcp(S.dK[j] - di);
+    }
+    const double zi = S.zK[S.idx[i]];
+    const double mag = sqrt(fabs(prod));
+    S.zh[i] = (zi < 0.0) ? -mag : mag;
+  }
+  __syncwarp();
+  // all eigenvalues: non-deflated roots, then deflated poles in coordinate order
+  for (int q = lane; q < m; q += 32) {
+    double lv;
+    if (q < K) {
+      lv = S.ls[q] + S.lt[q];
+      S.kind[q] = q;
+    } else {
+      int cnt = 0, coord = 0;
+      for (int a = 0; a < m; ++a)
+        if (S.flag[a]) {
+          if (cnt == q - K) {
+            coord = a;
+            break;
+          }
+          ++cnt;
+        }
+      lv = S.dwork[coord];
+      S.kind[q] = kWide + coord;
+    }
+    S.lamall[q] = lv;
+  }
+  __syncwarp();
+  for (int q = lane; q < m; q += 32) {
+    const double li = S.lamall[q];
+    int rk = 0;
+    for (int j = 0; j < m; ++j) {
+      const double lj = S.lamall[j];
+      if (lj > li || (lj == li && j < q)) ++rk;
+    }
+    S.perm[rk] = q;
+  }
+  __syncwarp();
+  // eigenvector columns, sign rule, clamp
+  for (int col = lane; col < m; col += 32) {
+    const int src = S.perm[col];
+    const int kind = S.kind[src];
+    for (int a = 0; a < m; ++a) S.sW[a * PW + col] = 0.0;
+    if (kind < kWide) {
+      const int j = kind;
+      double nrm2 = 0.0;
+      for (int i = 0; i < K; ++i) {
+        const double t = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]);
+        nrm2 += t * t;
+      }
+      const double inv = 1.0 / sqrt(nrm2);
+      if (!sh_rot) {
+        for (int i = 0; i < K; ++i)
+          S.sW[S.idx[i] * PW + col] = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
+      } else {
+        for (int i = 0; i < K; ++i) {
+          const double c = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
+          const int coord = S.idx[i];
+          for (int a = 0; a < m; ++a) S.sW[a * PW + col] += S.sQ[a * PW + coord] * c;
+        }
+      }
+    } else {
+      const int coord = kind - kWide;
+      for (int a = 0; a < m; ++a) S.sW[a * PW + col] = S.sQ[a * PW + coord];
+    }
+    int arg = 0;
+    double best = fabs(S.sW[col]);
+    for (int a = 1; a < m; ++a) {
+      const double av = fabs(S.sW[a * PW + col]);
+      if (av > best) {
+        best = av;
+        arg = a;
+      }
+    }
+    const bool flip = S.sW[arg * PW + col] < 0.0;
+    for (int a = 0; a < m; ++a) {
+      const double v = flip ? -S.sW[a * PW + col] : S.sW[a * PW + col];
+      W[a + col * m] = v;
+    }
+    const double lv = S.lamall[src];
+    lam[col] = lv < 0.0 ? 0.0 : lv;
+  }
+  __syncwarp();
+  return iters;
+}
+
 // Register-resident variant for m <= KM: the deflation scan, root solve,
 // Loewner z-hat and eigenvectors run lane-parallel over unrolled register
 // arrays (no shared-memory loops on the critical path). Close poles (which

@@ -273,6 +273,13 @@ class StreamingState:
         if isinstance(y, np.ndarray) and y.ndim > 1:
             y, _ = _flat(y)
         ptr, kind = _pointer(y)
+        # the pipelined engine may read a slice again until two further updates
+        # have returned (include/tsg.h): keep the last inputs alive here
+        live = getattr(self, "_live", None)
+        if live is None:
+            live = self._live = []
+        live.append(y)
+        del live[:-4]
         self._check(self.L.tsg_update(self.h, ptr, kind))
 
     def update_device_ptr(self, ptr: int):
@@ -284,6 +291,8 @@ class StreamingState:
 
     def synchronize(self):
         self._check(self.L.tsg_synchronize(self.h))
+        if getattr(self, "_live", None):
+            self._live.clear()
 
     def process_nonstreaming_mode(self, y: np.ndarray, mode: int, delta: float):
         x, dims = _flat(y)

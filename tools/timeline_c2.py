@@ -10,16 +10,26 @@ cfg = dg.CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 gen = dg.make_stream(cfg)
 dev = torch.device("cuda", 0)
 init = torch.cat([gen.slice_torch(t, dev) for t in range(cfg.n_init)])
-ys = [gen.slice_torch(cfg.n_init + i, dev) for i in range(50)]
+skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # untimed updates before the window
 st = S.StreamingState(device=0, asynchronous=True, profile=True)
 st.init_flat(init, gen.init_dims(), cfg.tau)
+del init
+for i in range(skip):
+    st.stream_update(gen.slice_torch(cfg.n_init + i, dev))
+    if i % 8 == 7:
+        st.synchronize()
+st.synchronize()
+ys = [gen.slice_torch(cfg.n_init + skip + i, dev) for i in range(50)]
 for y in ys[:20]:
     st.stream_update(y)
 st.synchronize()
 st.profile(reset=True)
+import time
+t0 = time.perf_counter()
 for y in ys[20:]:
     st.stream_update(y)
 st.synchronize()
+print("host wall per update: %.1f us; ranks %s" % ((time.perf_counter() - t0) / 30 * 1e6, st.query()["core_dims"]))
 t = st.timeline() * 1e3
 t -= t[0, 0]
 print("slice  m0_start  m0_end  decision  isvd_start  isvd_end | m0  tail  dec->isvd  isvd  isvd_gap")
