@@ -368,7 +368,8 @@ def run_ours(args, world, rank, local):
         achieved = flops / t_mode0 / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": dmma, "unit": "TFLOP/s",
                 "frac": achieved / dmma, "peak_source": "measured FP64 DMMA (tsg_measure_fp64_peaks)"}
-    roof["kernel"] = "proj0_tma_kernel (mode-0 projection + residual norm)"
+    roof["kernel"] = ("mode-0 fused projection + residual norm (proj0_colsr_kernel: column-owning DMMA, "
+                      "bulk-copy ring; proj0_tma_kernel / proj_dmma_kernel outside its envelope)")
     roof["algorithmic_bytes_per_launch"] = nbytes
     roof["algorithmic_flops_per_launch"] = flops
     roof["avg_launch_ms"] = prof["mode0_ms"]

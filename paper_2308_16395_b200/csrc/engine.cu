@@ -206,6 +206,7 @@ struct tsg_stream {
       GraphEntry g;
       const long long l0 = g_launches;
       cap_xnode = nullptr;
+      const auto cap_t0 = std::chrono::steady_clock::now();
       ck(cudaStreamBeginCapture(s_, cudaStreamCaptureModeRelaxed), "cudaStreamBeginCapture");
       try {
         body(true);
@@ -229,6 +230,10 @@ struct tsg_stream {
         fail(TSG_EDEVICE, "graph capture: slice-reading kernel node not found");
       }
       it = graphs.emplace(key, g).first;
+      if (growth_clk) {
+        gclk[6] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - cap_t0).count();
+        ++gcnt[6];
+      }
     }
     GraphEntry& ge = it->second;
     if (ge.xnode && ge.pa.x != x) {
@@ -342,6 +347,34 @@ struct tsg_stream {
   std::vector<std::pair<void*, long long>> allocs;
   long long launches_at_create = 0;
 
+  // TSG_GROWTH_CLK=1: host wall-clock breakdown of the slow path (stderr)
+  bool growth_clk = std::getenv("TSG_GROWTH_CLK") != nullptr;
+  double gclk[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long gcnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  std::chrono::steady_clock::time_point gt0;
+  void gtic() {
+    if (growth_clk) {
+      sync();
+      gt0 = std::chrono::steady_clock::now();
+    }
+  }
+  void gtoc(int i) {
+    if (!growth_clk) return;
+    sync();
+    gclk[i] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - gt0).count();
+    ++gcnt[i];
+    gt0 = std::chrono::steady_clock::now();
+  }
+  void gdump() {
+    if (!growth_clk) return;
+    static const char* nm[8] = {"rebuild-proj", "residual", "gram+eig", "finish(carried,pad,concat)",
+                                "re-decide", "insert", "graph-capture", "slow-path total"};
+    for (int i = 0; i < 8; ++i)
+      if (gcnt[i])
+        std::fprintf(stderr, "growth clk: %-28s x%5lld  %9.3f ms total  %8.3f ms avg\n", nm[i], gcnt[i],
+                     gclk[i], gclk[i] / gcnt[i]);
+  }
+
   // ------------------------------------------------------------ memory
   // Freed blocks up to kPoolBlockMax are kept (by capacity) and handed out
   // again: the growth path allocates the same temporaries for every basis
@@ -408,6 +441,8 @@ struct tsg_stream {
     cudaFree(p);
   }
   void free_all() {
+    gdump();
+    for (int i = 0; i < 8; ++i) gclk[i] = 0, gcnt[i] = 0;
     if (st) cudaStreamSynchronize(st);
     if (si) cudaStreamSynchronize(si);
     if (sc) cudaStreamSynchronize(sc);
@@ -797,10 +832,14 @@ struct tsg_stream {
   // `dst` (concat of p and the carried coefficients), yd updated.
   void expand_mode(const double* y, long long* yd, int mode, double delta, double* p,
                    double* dst) {
+    gtic();
     expand_residual(y, yd, mode, p);
+    gtoc(1);
     Sub s = mode_subspace(ebuf, yd, d - 1, mode, delta);
     dbg("expand: mode_subspace");
+    gtoc(2);
     expand_finish(yd, mode, s, p, dst);
+    gtoc(3);
   }
   // First half: P = U^T Y into p, residual E = Y - U P into ebuf.
   void expand_residual(const double* y, const long long* yd, int mode, double* p) {
@@ -1215,6 +1254,7 @@ struct tsg_stream {
   // host-orchestrated path (streaming.cpp:171-185, 140-151).
   void update_slow(const double* y, int par, std::chrono::steady_clock::time_point t0) {
     sync();
+    const auto s0 = std::chrono::steady_clock::now();
     drain(true);
     pull_ctrl();
     const SliceCtl sc = hslot[par];
@@ -1225,6 +1265,11 @@ struct tsg_stream {
     long long yd[kMaxD];
     for (int k = 0; k + 1 < d; ++k) yd[k] = N[k];
     run_growth(y, yd, 0, sc.expand_mode, sc.delta, par, t0);
+    if (growth_clk) {
+      sync();
+      gclk[7] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - s0).count();
+      ++gcnt[7];
+    }
   }
 
   // streaming.cpp:171-185: a zero left row and a metrics record.
@@ -1268,6 +1313,7 @@ struct tsg_stream {
     const double* b = nullptr;
     while (true) {
       // rebuild the input of mode em from `base` (same kernels, same data)
+      gtic();
       const double* cur = base;
       for (int k = m0; k < em; ++k) {
         double* out = pick(cur, base);
@@ -1275,6 +1321,7 @@ struct tsg_stream {
         yd[k] = R[k];
         cur = out;
       }
+      gtoc(0);
       double* pbuf = pick(cur, base);
       double* dst = pick(cur, pbuf);
       expand_mode(cur, yd, em, delta, pbuf, dst);
@@ -1301,6 +1348,7 @@ struct tsg_stream {
       da.first_mode = m0;
       launch_decide(da, st);
       pull_slot(par);
+      gtoc(4);
       em = slots_h[par].expand_mode;
       if (em < 0) {
         launch_commit_modes(ctrl, slots + par, m0, d - 1, 0, st);
@@ -1311,9 +1359,11 @@ struct tsg_stream {
     }
     pull_ctrl();
     r_exact = ctrl_h->r;
+    gtic();
     ensure_pipe();
     enqueue_isvd(b, par, mask, st, false, t0);
     ck(cudaEventRecord(ev_proj[par], st), "cudaEventRecord");
+    gtoc(5);
   }
 
   // ------------------------------------------------------ sharded update

@@ -439,6 +439,55 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
   const int rank = sh_rank;
   double* U = io.inner + L.U;
   for (int j = threadIdx.x; j < rank; j += blockDim.x) io.sigma_new[j] = sqrt(lam[j]);
+  if (use_wide) {
+    // U = S' W / sigma and its MGS pass in shared memory (the secular
+    // scratch is free now), a warp per column with lanes over the rows
+    double* sU = wide;  // rows x rank, ld rows (<= 65 x 64)
+    for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) {
+      const int i = idx % rows, j = idx / rows;
+      double s = 0.0;
+      if (i < r) {
+        s = io.sigma[i] * W[i + j * m];                   // rows i < r of S' are diag(s)
+      } else {
+        for (int l = 0; l < m; ++l) s += Sp(io, r, l) * W[l + j * m];
+      }
+      sU[i + j * rows] = s * (1.0 / sqrt(lam[j]));
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int i = 0; i < rank; ++i) {
+      double* ui = sU + i * rows;
+      if (wid == 0) {
+        double ss = 0.0;
+        for (int l = lane; l < rows; l += 32) ss += ui[l] * ui[l];
+        ss = warp_sum(ss);
+        const double nrm = sqrt(ss);
+        if (nrm > 0.0)
+          for (int l = lane; l < rows; l += 32) ui[l] /= nrm;
+      }
+      __syncthreads();
+      for (int j = i + 1 + wid; j < rank; j += nw) {
+        double* uj = sU + j * rows;
+        double dot = 0.0;
+        for (int l = lane; l < rows; l += 32) dot += ui[l] * uj[l];
+        dot = warp_sum(dot);
+        for (int l = lane; l < rows; l += 32) uj[l] -= dot * ui[l];
+      }
+      __syncthreads();
+    }
+    for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) U[idx] = sU[idx];
+    double* M = io.inner + L.M;
+    double* w = io.inner + L.w;
+    for (int idx = threadIdx.x; idx < rank * r; idx += blockDim.x) {
+      const int jn = idx % rank, j = idx / rank;
+      double s = 0.0;
+      for (int l = 0; l < r; ++l) s += sU[l + jn * rows] * io.pgram[l + j * r];
+      M[jn + j * rank] = s;
+    }
+    for (int j = threadIdx.x; j < rank; j += blockDim.x) w[j] = sU[r + j * rows];
+    __syncthreads();
+    return;
+  }
   for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) {
     const int i = idx % rows, j = idx / rows;
     double s = 0.0;
@@ -1056,6 +1105,88 @@ __global__ void __launch_bounds__(256) isvd_update_kernel(const Ctrl* ctrl, cons
   }
 }
 
+// Split-path row update with the small factors in shared memory: a thread
+// owns a row and keeps its 2 x RN outputs in registers while it streams the
+// row's r entries of Q and of the core once (coalesced over the rows); W and
+// M^T are read as warp-wide broadcasts (ld.shared.v2). Each output is the same
+// l-ordered sum as update_rows (bit-identical), without its LDG per FMA and
+// its 2 x RMAX register row copies: 128 -> ~20 us at n = 46656, r = 36.
+// RN >= r_new (zero-padded columns).
+template <int RN>
+__global__ void __launch_bounds__(128) isvd_update_acc_kernel(
+    const Ctrl* ctrl, const double* __restrict__ q, const double* __restrict__ cin,
+    const double* __restrict__ e, const double* __restrict__ b, const double* __restrict__ inner,
+    const double* __restrict__ sigma_new, long long n, int capr, double* __restrict__ qn,
+    double* __restrict__ cn, double* __restrict__ part) {
+  extern __shared__ double usm[];  // sW (r+1) x RN | sM r x RN | sw RN | ssig RN
+  __shared__ double red[32];
+  const InnerLayout L = inner_layout(capr);
+  const int r = ctrl->r, rn = ctrl->r_new, deg = ctrl->degenerate;
+  const int m = deg ? r : r + 1;
+  const double* W = inner + L.W;
+  const double* M = inner + L.M;
+  const double* w = inner + L.w;
+  double* sW = usm;
+  double* sM = sW + (r + 1) * RN;
+  double* sw = sM + r * RN;
+  double* ssig = sw + RN;
+  for (int idx = threadIdx.x; idx < (r + 1) * RN; idx += blockDim.x) {
+    const int l = idx / RN, jn = idx % RN;
+    sW[idx] = (jn < rn && l < m) ? W[l + jn * m] : 0.0;
+  }
+  for (int idx = threadIdx.x; idx < r * RN; idx += blockDim.x) {
+    const int l = idx / RN, jn = idx % RN;
+    sM[idx] = jn < rn ? M[jn + l * rn] : 0.0;
+  }
+  for (int jn = threadIdx.x; jn < RN; jn += blockDim.x) {
+    sw[jn] = jn < rn ? w[jn] : 0.0;
+    ssig[jn] = jn < rn ? sigma_new[jn] : 0.0;
+  }
+  __syncthreads();
+  const double inv = deg ? 0.0 : 1.0 / sqrt(ctrl->e_sq);
+  double dacc = 0.0, cacc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    double sq[RN], sc[RN];
+#pragma unroll
+    for (int jn = 0; jn < RN; ++jn) sq[jn] = sc[jn] = 0.0;
+    for (int l = 0; l < r; ++l) {
+      const double qv = q[i + (long long)l * n];
+      const double cv = cin[i + (long long)l * n];
+      const double2* wr = reinterpret_cast<const double2*>(sW + l * RN);
+      const double2* mr = reinterpret_cast<const double2*>(sM + l * RN);
+#pragma unroll
+      for (int jn = 0; jn < RN / 2; ++jn) {
+        const double2 wv = wr[jn], mv = mr[jn];
+        sq[2 * jn] += qv * wv.x;
+        sq[2 * jn + 1] += qv * wv.y;
+        sc[2 * jn] += cv * mv.x;
+        sc[2 * jn + 1] += cv * mv.y;
+      }
+    }
+    const double qi = deg ? 0.0 : e[i] * inv;
+    const double bi = b[i];
+#pragma unroll
+    for (int jn = 0; jn < RN; ++jn) {
+      if (!deg) sq[jn] += qi * sW[r * RN + jn];
+      sc[jn] += sw[jn] * bi;
+      if (jn < rn) {
+        qn[i + (long long)jn * n] = sq[jn];
+        cn[i + (long long)jn * n] = sc[jn];
+        const double diff = sc[jn] - sq[jn] * ssig[jn];
+        dacc += diff * diff;
+        cacc += sc[jn] * sc[jn];
+      }
+    }
+  }
+  dacc = block_sum(dacc, red);
+  cacc = block_sum(cacc, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = dacc;
+    part[2 * blockIdx.x + 1] = cacc;
+  }
+}
+
 __global__ void isvd_left_kernel(const Ctrl* ctrl, const double* __restrict__ left, int capr,
                                  const double* __restrict__ inner,
                                  double* __restrict__ left_new) {
@@ -1339,13 +1470,50 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   double* part3 = part2 + (long long)nb * (capr + 1);
   double* part4 = part3 + nb;
   const InnerLayout L = inner_layout(capr);
+  // TSG_SPLIT_CLK=1 (with TSG_NO_GRAPH=1): CUDA events between the split
+  // kernels, averages printed every 32 insertions (diagnostic only)
+  static const bool clk = std::getenv("TSG_SPLIT_CLK") != nullptr;
+  static cudaEvent_t cev[10];
+  static double cacc[10];
+  static int ccount = 0;
+  static bool cinit = false, clive = false;
+  auto mark = [&](int i) {
+    if (!clk) return;
+    cudaEventRecord(cev[i], st);
+  };
+  if (clk) {
+    if (!cinit) {
+      for (auto& e : cev) cudaEventCreate(&e);
+      cinit = true;
+    }
+    if (clive) {
+      cudaEventSynchronize(cev[9]);
+      for (int i = 0; i < 9; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, cev[i], cev[i + 1]);
+        cacc[i] += ms;
+      }
+      if (++ccount % 32 == 0) {
+        static const char* nm[9] = {"pgram", "pass1", "pass2", "pass3", "inner", "update", "left", "finalize", "-"};
+        std::fprintf(stderr, "split insertion (n %lld, capr %d), avg us:", n, capr);
+        for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %s %.1f", nm[i], cacc[i] / ccount * 1e3);
+        std::fprintf(stderr, "\n");
+      }
+    }
+    clive = true;
+  }
+  mark(0);
   pgram_kernel<<<1, 1024, sizeof(double) * 2 * kPgTile * capr, st>>>(B.ctrl, B.left, capr,
                                                                      B.inner + L.pg);
+  mark(1);
   isvd_pass1_kernel<<<nb, 256, 0, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr, part1);
+  mark(2);
   isvd_pass2_kernel<<<nb, 256, sizeof(double) * capr, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr,
                                                             nb, part1, B.e, part2);
+  mark(3);
   isvd_pass3_kernel<<<nb, 256, sizeof(double) * capr, st>>>(B.ctrl, B.q, n, rows_per, capr, nb,
                                                             part2, B.e, part3);
+  mark(4);
   InnerArgs ia;
   ia.ctrl = B.ctrl;
   ia.slot = B.slot;
@@ -1367,8 +1535,26 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   if (ia.wide) smem = std::max(smem, sizeof(double) * (size_t)kWideScratch);
   ensure_smem(isvd_inner_kernel, smem);
   isvd_inner_kernel<<<1, 512, smem, st>>>(ia);
-  const int gu = grid_for(n, 256, 148 * 4);
-  if (capr <= 16)
+  mark(5);
+  int gu = grid_for(n, 256, 148 * 4);
+  static const bool old_update = std::getenv("TSG_OLD_UPDATE") != nullptr;  // A/B
+  const int rn_max = B.r_hint + 1;  // r_new <= r + 1 <= r_hint + 1
+  if (!old_update && rn_max <= 48 && B.r_hint >= 1) {
+    gu = grid_for(n, 128, 148 * 4);
+    const size_t usm = sizeof(double) * ((size_t)(2 * rn_max + 1) * 48 + 96);
+#define TSG_UPD(RN)                                                                          \
+  {                                                                                          \
+    ensure_smem(isvd_update_acc_kernel<RN>, usm);                                            \
+    isvd_update_acc_kernel<RN><<<gu, 128, usm, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner,    \
+                                                     B.sigma_new, n, capr, B.qn, B.cn, part4); \
+  }
+    if (rn_max <= 16) TSG_UPD(16)
+    else if (rn_max <= 24) TSG_UPD(24)
+    else if (rn_max <= 32) TSG_UPD(32)
+    else if (rn_max <= 40) TSG_UPD(40)
+    else TSG_UPD(48)
+#undef TSG_UPD
+  } else if (capr <= 16)
     isvd_update_kernel<16><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
                                                capr, B.qn, B.cn, part4);
   else if (capr <= 32)
@@ -1380,9 +1566,13 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
   else
     isvd_update_kernel<0><<<gu, 256, 0, st>>>(B.ctrl, B.q, B.c, B.e, B.b, B.inner, B.sigma_new, n,
                                               capr, B.qn, B.cn, part4);
+  mark(6);
   isvd_left_kernel<<<grid_for(B.cap_rows * capr), 256, 0, st>>>(B.ctrl, B.left, capr, B.inner,
                                                                  B.left_new);
+  mark(7);
   isvd_finalize_kernel<<<1, 256, 0, st>>>(B.ctrl, B.slot, part4, gu, B.ring, B.order, sr);
+  mark(8);
+  mark(9);
   g_launches += 8;
 }
 

@@ -11,7 +11,7 @@ gen = dg.make_stream(cfg)
 dev = torch.device("cuda", 0)
 init = torch.cat([gen.slice_torch(t, dev) for t in range(cfg.n_init)])
 skip = int(sys.argv[2]) if len(sys.argv) > 2 else 0   # untimed updates before the window
-st = S.StreamingState(device=0, asynchronous=True, profile=True)
+st = S.StreamingState(device=0, asynchronous=os.environ.get("TL_SYNC") is None, profile=True)
 st.init_flat(init, gen.init_dims(), cfg.tau)
 del init
 for i in range(skip):
