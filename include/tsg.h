@@ -130,6 +130,26 @@ int tsg_process_mode(tsg_stream* h, const double* y, const int64_t* ydims,
                      int32_t mode, double delta, double* y_out,
                      int64_t y_out_cap, int64_t* ydims_out, double* res);
 
+/* add_row (isvd.hpp:110-111; isvd.cpp:163-250) on the device-resident ISVD of
+ * the handle, together with the core rotation stream_update applies around it
+ * (streaming.cpp:199-222): b holds n = R_0 * ... * R_{d-2} doubles (the
+ * vectorised projected slice), abs_tol is the explicit truncation threshold
+ * (stream_update passes delta = tau ||y|| / sqrt(d)), slice_norm_sq >= 0 is
+ * added to total_input_sq (streaming.cpp:169; pass 0 to leave it alone).
+ * One stream_update equals tsg_process_mode for every non-streaming mode
+ * followed by this call. The result mirrors AddRowResult (isvd.hpp:97-104)
+ * without inner_left, whose only use — the core rotation — is done here.
+ * isvd_init (isvd.hpp:91-93) is tsg_import_state: a 2-way state whose single
+ * factor is the identity is exactly a stand-alone ISVDState (left, singular
+ * values, right = the core's column space), see INTEGRATION.md. */
+typedef struct {
+  int64_t r_old, r_new;
+  int32_t degenerate;        /* residual too small to add a direction */
+  double added_error_sq;     /* energy the inner truncation discarded */
+} tsg_add_row_result;
+int tsg_add_row(tsg_stream* h, const double* b, int32_t mem_kind, double abs_tol,
+                double slice_norm_sq, tsg_add_row_result* out);
+
 int tsg_query(tsg_stream* h, tsg_dims* out);
 int tsg_export_state(tsg_stream* h, double* core, double* factors,
                      double* sigma, double* left, double* right);

@@ -2183,6 +2183,46 @@ struct tsg_stream {
   }
 
   // process_nonstreaming_mode (streaming.cpp:126-155) on a host tensor.
+  // add_row (isvd.hpp:110-111, isvd.cpp:163-250) on the device state, with
+  // the core rotation stream_update applies around it (streaming.cpp:199-222):
+  // b = vec(projected slice), n = prod R_k entries; abs_tol is the explicit
+  // truncation threshold; slice_sq (>= 0) is booked into total_input_sq.
+  // stream_update == process_nonstreaming_mode for every mode + this call.
+  void add_row(const double* b_in, int mem_kind, double abs_tol, double slice_sq,
+               tsg_add_row_result* out) {
+    if (!initialized) fail(TSG_EINVAL, "add_row: state not initialised");
+    if (!(abs_tol >= 0.0) || !(slice_sq >= 0.0)) fail(TSG_EINVAL, "add_row: negative threshold or norm");
+    flush();
+    const long long n = n_rows();
+    double* bd = w0;  // >= slice_elems >= n doubles
+    ck(cudaMemcpyAsync(bd, b_in, sizeof(double) * n,
+                       mem_kind == TSG_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, st),
+       "row copy");
+    SliceCtl sc;
+    std::memset(&sc, 0, sizeof sc);
+    sc.slice_sq = slice_sq;
+    sc.delta = abs_tol;
+    sc.expand_mode = -1;
+    slots_h[0] = sc;
+    ck(cudaMemcpyAsync(slots, slots_h, sizeof(SliceCtl), cudaMemcpyHostToDevice, st), "slot H2D");
+    launch_commit_modes(ctrl, slots, 0, 0, 1, st);  // total_input_sq += slice_sq
+    const int r_old = ctrl_h->r;
+    r_exact = r_old;
+    ensure_pipe();
+    enqueue_isvd(bd, 0, 0, st, false, std::chrono::steady_clock::now());
+    sync();
+    drain(true);
+    pull_ctrl();
+    r_exact = ctrl_h->r;
+    if (out) {
+      out->r_old = r_old;
+      out->r_new = ctrl_h->r;
+      out->degenerate = ctrl_h->degenerate;
+      out->added_error_sq = ctrl_h->added_error_sq;
+    }
+    check_status();
+  }
+
   double process_mode(const double* y_h, const long long* ydims, int mode, double delta,
                       double* y_out, long long cap, long long* ydims_out) {
     if (mode < 0 || mode >= d - 1) fail(TSG_EINVAL, "process_mode: mode out of range");
@@ -2419,6 +2459,14 @@ int tsg_process_mode(tsg_stream* h, const double* y, const int64_t* ydims, int32
     for (int k = 0; k + 1 < h->d; ++k) yd[k] = ydims[k];
     *res = h->process_mode(y, yd, mode, delta, y_out, y_out_cap, od);
     for (int k = 0; k + 1 < h->d; ++k) ydims_out[k] = od[k];
+  });
+}
+
+int tsg_add_row(tsg_stream* h, const double* b, int32_t mem_kind, double abs_tol,
+                double slice_norm_sq, tsg_add_row_result* out) {
+  return guarded(h, [&] {
+    if (!b) fail(TSG_EINVAL, "tsg_add_row: row must not be null");
+    h->add_row(b, mem_kind, abs_tol, slice_norm_sq, out);
   });
 }
 

@@ -93,6 +93,12 @@ class TsgExchange(C.Structure):
 XCHG_ALLGATHER, XCHG_ALLREDUCE_SUM = 0, 1
 
 
+class TsgAddRowResult(C.Structure):
+    """tsg_add_row_result (AddRowResult, isvd.hpp:97-104, without inner_left)."""
+    _fields_ = [("r_old", C.c_int64), ("r_new", C.c_int64), ("degenerate", C.c_int32),
+                ("added_error_sq", C.c_double)]
+
+
 class TsgMetrics(C.Structure):
     _fields_ = [
         ("slice_index", C.c_int64), ("ranks", C.c_int64 * MAXD),
@@ -110,7 +116,7 @@ EXPORTED = [
     "tsg_kernel_launches", "tsg_cuda_stream", "tsg_slice_buffer", "tsg_sym_eig_desc",
     "tsg_small_svd_truncated", "tsg_mode_subspace", "tsg_ttm", "tsg_profile",
     "tsg_measure_fp64_peaks", "tsg_readback_bytes_per_update", "tsg_debug_project",
-    "tsg_shard_setup", "tsg_shard_setup_mode", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
+    "tsg_add_row", "tsg_shard_setup", "tsg_shard_setup_mode", "tsg_shard_begin", "tsg_shard_continue", "tsg_reconstruct",
     "tsg_error_sums", "tsg_profile_timeline", "tsg_save_checkpoint", "tsg_load_checkpoint",
 ]
 
@@ -164,6 +170,8 @@ def load_library(path: str = LIB_PATH) -> C.CDLL:
     L.tsg_readback_bytes_per_update.argtypes = []
     L.tsg_readback_bytes_per_update.restype = C.c_int64
     L.tsg_shard_setup.argtypes = [C.c_void_p, C.c_int32, C.c_int32, _i64p]
+    L.tsg_add_row.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_double, C.c_double,
+                              C.POINTER(TsgAddRowResult)]
     L.tsg_shard_setup_mode.argtypes = [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _i64p]
     L.tsg_shard_begin.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(TsgExchange)]
     L.tsg_shard_continue.argtypes = [C.c_void_p, C.POINTER(TsgExchange)]
@@ -281,6 +289,19 @@ class StreamingState:
         live.append(y)
         del live[:-4]
         self._check(self.L.tsg_update(self.h, ptr, kind))
+
+    def add_row(self, b, abs_tol: float, slice_norm_sq: float = 0.0) -> dict:
+        """add_row (isvd.hpp:110-111) on the device ISVD plus the core rotation of
+        stream_update (streaming.cpp:199-222): b = vec(projected slice), n doubles
+        (numpy or CUDA torch). Returns r_old, r_new, degenerate, added_error_sq."""
+        if isinstance(b, np.ndarray):
+            b = np.ascontiguousarray(b.ravel(order="F"), dtype=np.float64)
+        ptr, kind = _pointer(b)
+        res = TsgAddRowResult()
+        self._check(self.L.tsg_add_row(self.h, ptr, kind, float(abs_tol), float(slice_norm_sq),
+                                       C.byref(res)))
+        return {"r_old": int(res.r_old), "r_new": int(res.r_new),
+                "degenerate": bool(res.degenerate), "added_error_sq": float(res.added_error_sq)}
 
     def update_device_ptr(self, ptr: int):
         self._check(self.L.tsg_update(self.h, C.c_void_p(ptr), MEM_DEVICE))

@@ -164,3 +164,44 @@ def test_checkpoint_loader_errors(tmp_path):
     bad.write_bytes(bytes(raw))
     with pytest.raises(S.CouplingDrift):
         S.load_checkpoint(str(bad))
+
+
+@pytest.mark.parametrize("name", ["growth24", "c3_40", "order5", "order2"])
+def test_add_row_composes_stream_update(oracle, name):
+    """tsg_add_row (add_row, isvd.hpp:110-111 / isvd.cpp:163-250, plus the core
+    rotation of streaming.cpp:199-222): one stream_update equals
+    process_nonstreaming_mode for every mode followed by add_row with
+    delta = tau ||y|| / sqrt(d) (the reference's own decomposition,
+    streaming.cpp:187-200). The composed state matches the one-call state to
+    rounding and the CPU checker to the parity bounds; AddRowResult's fields
+    follow the ranks."""
+    case = cases.STREAM_CASES[name]()
+    n = min(len(case.slices), 14)
+    one = _gpu(case, n=n)
+    st = S.StreamingState()
+    st.init_flat(case.init_flat, case.init_dims, case.tau)
+    dims = tuple(case.init_dims[:-1])
+    d = len(case.init_dims)
+    for y in case.slices[:n]:
+        t = y.reshape(dims[::-1]).transpose()
+        nrm = float(np.linalg.norm(y))
+        delta = case.tau * nrm / np.sqrt(d)
+        cur = t
+        for k in range(d - 1):
+            _, cur = st.process_nonstreaming_mode(cur, k, delta)
+        r_before = st.query()["rank"]
+        res = st.add_row(cur, delta, slice_norm_sq=nrm * nrm)
+        assert res["r_old"] == r_before and res["r_new"] == st.query()["rank"]
+        assert res["r_new"] <= res["r_old"] + 1 and res["added_error_sq"] >= 0.0
+    a, b = st.export(), one.export()
+    assert a.core_dims == b.core_dims and a.n_d == b.n_d
+    sc = P.compare_states(a, b)
+    print(name, "composed vs one call", sc)
+    assert sc["core"] <= 1e-11 and sc["sigma"] <= 1e-12 and sc["factors"] <= 1e-11
+    assert sc["ledger_sq_err"] <= 1e-13 and sc["ledger_nonstream"] <= 1e-13 and sc["ledger_total"] <= 1e-14
+    so = _checker(oracle, case, n=n).export()
+    P.assert_parity({"rank_mismatch_steps": [], "expanded_mask_equal": True, "slice_norm": 0.0,
+                     "projected_norm": 0.0, "mode_residuals": 0.0, "booked": 0.0},
+                    P.compare_states(a, so))
+    with pytest.raises(S.InvalidArgument):
+        st.add_row(np.zeros(int(np.prod(a.core_dims[:-1]))), -1.0)
