@@ -502,6 +502,9 @@ def run_sharded(args, world, rank, local):
     ms = allreduce_max(world, e0.elapsed_time(e1))
     q = st.query()
     value = args.steps / (ms / 1e3)
+    exchange = {"collectives_per_step": (st.exchanges - ex0) / args.steps,
+                "bytes_received_per_rank_per_step":
+                    8.0 * (st.exchanged_doubles - xd0) / args.steps}
     # roofline of the dominant kernel work: the LOCAL projection pass of the
     # slab (modes before the shard mode), event-timed on the engine's stream
     # over a few extra updates (begin = local pass enqueued; the events
@@ -563,9 +566,7 @@ def run_sharded(args, world, rank, local):
                 "shard_mode": st.mode, "shard_rows": list(bounds),
                 "l2": "each step reads a distinct device-resident slab (never re-read)",
                 "mode": "sharded engine: local modes, one allgather per slice, redundant finish"},
-        "exchange": {"allgathers_per_step": (st.exchanges - ex0) / args.steps,
-                     "bytes_gathered_per_rank_per_step":
-                         8.0 * (st.exchanged_doubles - xd0) / args.steps / world},
+        "exchange": exchange,
         "clocks": clk, "gpu_launches": st.kernel_launches() - launches0,
         "e2e": e2e, "cpu_baseline": cpu, "roofline": roof,
     }
