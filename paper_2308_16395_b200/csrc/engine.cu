@@ -1062,7 +1062,7 @@ struct tsg_stream {
   // enqueues the projections of slice t+2 BEFORE it waits for the decision of
   // slice t, so the projection stream always holds queued work (with one
   // deferred slice the period was (decision latency + host turnaround) / 2).
-  static constexpr int kDefer = 2;
+  static constexpr int kDefer = kNP - 1;
   std::vector<Pend> deferred;
   // Act on the oldest deferred slices until at most `keep` remain; when a slow
   // path ran (bases may have grown), the younger ones are projected again.
