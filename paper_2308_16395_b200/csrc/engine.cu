@@ -889,12 +889,17 @@ struct tsg_stream {
     ModeView cv{prod(cd, mode), R[mode], prod(cd + mode + 1, d - 1 - mode)};
     const long long n_new = n_rows() / R[mode] * (R[mode] + g);
     const long long new_qcap = n_new * capr;
-    double* nq = dalloc(new_qcap);
-    double* nc = dalloc(new_qcap);
+    // The out-of-place pad lands in the idle ping-pong buffers when they are
+    // large enough (no allocation per growth); otherwise all four buffers are
+    // re-allocated with room for further growth.
+    const bool in_spare = new_qcap <= qcap;
+    const long long alloc_qcap = in_spare ? qcap : 2 * new_qcap;
+    double* nq = in_spare ? Q2 : dalloc(alloc_qcap);
+    double* nc = in_spare ? core2 : dalloc(alloc_qcap);
     launch_pad(Q, cv, g, nq, st);
     launch_pad(core, cv, g, nc, st);
-    double* nq2 = dalloc(new_qcap);
-    double* nc2 = dalloc(new_qcap);
+    double* nq2 = in_spare ? Q : dalloc(alloc_qcap);
+    double* nc2 = in_spare ? core : dalloc(alloc_qcap);
     // ledger (streaming.cpp:150)
     double* dd = dalloc(1);
     ck(cudaMemcpyAsync(dd, &s.disc, 8, cudaMemcpyHostToDevice, st), "disc");
@@ -904,13 +909,15 @@ struct tsg_stream {
     dbg("expand: concat");
     sync();
     dfree(dd);
-    dfree(Q); dfree(Q2); dfree(core); dfree(core2);
+    if (!in_spare) {
+      dfree(Q); dfree(Q2); dfree(core); dfree(core2);
+    }
     Q = nq; Q2 = nq2; core = nc; core2 = nc2;
-    qcap = new_qcap;
+    qcap = alloc_qcap;
     if (e_alloc_n() < n_new) {
       dfree(evec);
-      evec = dalloc(n_new);
-      evec_n = n_new;
+      evec = dalloc(2 * n_new);
+      evec_n = 2 * n_new;
     }
     release(s);
     R[mode] += g;
@@ -935,12 +942,16 @@ struct tsg_stream {
     for (int k = 0; k + 1 < d; ++k) need *= (k == 0 ? R[0] : N[k]);
     if (need <= pipe_elems) return;
     sync();
+    // room for the leading basis to grow by half again (capped at its mode
+    // size) before the next re-allocation
+    long long room = need / std::max(1LL, R[0]) * std::min(N[0], R[0] + std::max(8LL, R[0] / 2));
+    room = std::max(room, need);
     for (auto& set : pw)
       for (auto& b : set) {
         dfree(b);
-        b = dalloc(need);
+        b = dalloc(room);
       }
-    pipe_elems = need;
+    pipe_elems = room;
   }
 
   // Enqueue the ISVD insertion + core rotation for the slice whose projected
