@@ -23,6 +23,7 @@
 #include "kernels.cuh"
 namespace tsg {
 __device__ long long g_isvd_clk[32];  // debug phase clocks (thread 0)
+__device__ long long g_isvd_acc[32];  // sums of (stamp - stamp 0) over insertions, [31] = count
 }
 #define SEC_CLK(i)                                         \
   do {                                                     \
@@ -58,6 +59,7 @@ __host__ __device__ inline InnerLayout inner_layout(int capr) {
 int isvd_inner_scratch(int capr) { return (int)inner_layout(capr).total; }
 
 int read_isvd_clocks(long long* out) {
+  if (out[0] == -12345) return cudaMemcpyFromSymbol(out, g_isvd_acc, sizeof(long long) * 32) == cudaSuccess ? 0 : 4;
   return cudaMemcpyFromSymbol(out, g_isvd_clk, sizeof(long long) * 32) == cudaSuccess ? 0 : 4;
 }
 

@@ -410,6 +410,11 @@ __global__ void __launch_bounds__(kT, 1) isvd_clu_kernel(IsvdBufs B, int R0) {
     if (lane == 0) *reinterpret_cast<volatile unsigned long long*>(&B.ring->done) = kr + 1;
   }
   TSG_CLK(9);
+  if (threadIdx.x == 0) {  // diagnostics: per-phase sums over all insertions
+    for (int i = 1; i < 24; ++i)
+      if (g_isvd_clk[i] >= g_isvd_clk[0]) g_isvd_acc[i] += g_isvd_clk[i] - g_isvd_clk[0];
+    g_isvd_acc[31] += 1;
+  }
 }
 
 }  // namespace clu
