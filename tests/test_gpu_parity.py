@@ -196,6 +196,29 @@ def test_growth_midsize_vs_oracle(oracle, size, every):
     P.assert_parity(mc, sc)
 
 
+@pytest.mark.parametrize("asynchronous", [False, True])
+def test_streaming_rank_past_32_vs_oracle(oracle, asynchronous):
+    """Streaming rank growing 6 -> 44: the insertion leaves the one-warp kernels
+    (r + 1 <= 32) for the split path, whose inner problems of 33..64 columns use
+    the wide secular solver and the shared-memory U / MGS (isvd.cu,
+    secular::eig_rank_one_wide), the tiled p_gram and the accumulator row-update
+    kernel. Per-step ranks identical, state within the parity bounds."""
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.StreamConfig("rank44", (40, 36), (10, 9), 44, 70, 6, 1e-3, 1e-5, 977,
+                          notes="3-way, time rank 44 (> 32)")
+    case = cases.config_case(cfg)
+    st = run_gpu(case, asynchronous=asynchronous)
+    ho = _oracle_run(oracle, case)
+    sg, so = st.export(), ho.export()
+    assert so.rank > 36, so.rank
+    mc = P.compare_metrics(P.metrics_arrays(st.metrics(), sg.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(sg, so)
+    print("rank", sg.rank, mc, sc)
+    P.assert_parity(mc, sc)
+    assert np.abs(sg.left.T @ sg.left - np.eye(sg.rank)).max() <= 1e-10
+
+
 @pytest.mark.slow
 def test_config3_generator_midsize_vs_oracle(oracle):
     """Config-3 generator (geometric core spectrum, R = 32) at 96^3."""
