@@ -165,7 +165,7 @@ __global__ void pad_u_kernel(const double* __restrict__ u, long long N, int R, i
 // The column-owning mode-0 kernel's two U images (proj0_cols.cuh), stored
 // right after the row-split image: image 1 (pitch 8RT+2) holds rank
 // 8nt+4i+t in column 8nt+2t+i, image 2 (pitch 8RT+4) natural rank order.
-__global__ void cols_u_kernel(const double* __restrict__ u, long long N, int R, int RT,
+__global__ void cols_u_kernel(const double* __restrict__ u, long long N, int R, int RT, int lo,
                               double* __restrict__ out) {
   const int p1 = 8 * RT + 2, p2 = 8 * RT + 4;
   const long long total = N * (p1 + p2);
@@ -181,7 +181,7 @@ __global__ void cols_u_kernel(const double* __restrict__ u, long long N, int R, 
       const long long j2 = idx - N * p1;
       row = j2 / p2;
       rk = (int)(j2 % p2);
-      if (rk >= 8 * RT) rk = R;
+      if (rk >= 8 * RT + lo) rk = R;  // lo left-over ranks follow the DMMA tiles (cols_lo)
     }
     out[idx] = rk < R ? u[row + rk * N] : 0.0;
   }
@@ -205,8 +205,8 @@ void launch_pad_u(const double* u, long long N, int R, double* out, cudaStream_t
   pad_u_kernel<<<(int)((rows8 * rpad + 255) / 256), 256, 0, st>>>(u, N, R, rpad, rows8, out);
   ++g_launches;
   if (N % 8 == 0) {
-    const int RT = (R + 7) / 8;
-    cols_u_kernel<<<(int)((N * (16 * RT + 6) + 255) / 256), 256, 0, st>>>(u, N, R, RT,
+    const int RT = cols0::cols_rt(N, R), lo = cols0::cols_lo(N, R);
+    cols_u_kernel<<<(int)((N * (16 * RT + 6) + 255) / 256), 256, 0, st>>>(u, N, R, RT, lo,
                                                                            out + rows8 * rpad);
     ++g_launches;
   }

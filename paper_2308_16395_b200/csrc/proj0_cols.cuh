@@ -53,6 +53,27 @@ __host__ __device__ inline long long upad_cols_offset_dev(long long N, int R) {
   return (N + 7) / 8 * 8 * (8 * ((R + 7) / 8) + 4);  // = upad_cols_offset (kernels_stream.cu)
 }
 
+// Ranks past the last full 8-rank DMMA tile that the register-resident kernel
+// computes on the FP64 FMA pipe instead of padding a whole rank tile with
+// zeros (R = 9..11 with N = 200 / 256: C2's R = 10 executes 75 + FMA work
+// instead of 175 DMMAs per 8 columns). DMMA and DFMA share one FP64 datapath
+// (profiles/r02/coissue_dmma_dfma.txt), so this only removes padded work.
+// The prebuilt U images (cols_u_kernel) follow the same rule.
+// MEASURED AND REJECTED as the default (TSG_COLS0_LO=1 enables it for A/B):
+// C2 mode 0 alone 30.4 us against 26.8 us with the padded second rank tile,
+// 37-39 us against 32 us inside the pipeline. Parity-clean either way. The
+// kernel is not FP64-datapath bound at 57 % DMMA-pipe utilisation: the extra
+// shared-memory operand loads and the issue slots of the 200 FMAs per tile
+// cost more than the 75 DMMAs they replace.
+inline int cols_lo(long long N, int R) {
+  static const bool on = [] {
+    const char* e = std::getenv("TSG_COLS0_LO");
+    return e ? std::atoi(e) != 0 : false;
+  }();
+  return (on && (N == 200 || N == 256) && R >= 9 && R <= 11) ? R - 8 : 0;
+}
+inline int cols_rt(long long N, int R) { return cols_lo(N, R) ? R / 8 : (R + 7) / 8; }
+
 template <int RT>
 __host__ __device__ constexpr int p1_pitch() { return 8 * RT + 2; }
 template <int RT>
@@ -269,7 +290,7 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_cols_kernel(ProjArgs a) {
 // from registers. One buffer per warp double-buffers in effect, so 12 warps
 // (3 per SM sub-partition, which the DMMA issue pattern needs) fit next to
 // the U images.
-template <int RT, int NW, int NG, bool HALF>
+template <int RT, int NW, int NG, bool HALF, int LO = 0>
 __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
   extern __shared__ __align__(128) double csm[];
   constexpr int P1 = p1_pitch<RT>(), P2 = p2_pitch<RT>();
@@ -331,10 +352,17 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
       U1[i * P1 + 8 * nt + 2 * tt + ii] = v;
       U2[i * P2 + rk] = v;
     }
+    for (int idx = threadIdx.x; idx < N * LO; idx += 32 * NW) {  // left-over ranks: image 2 only
+      const int l = idx / N, i = idx - l * N;
+      U2[i * P2 + 8 * RT + l] = a.u[(long long)(8 * RT + l) * N + i];
+    }
     __syncthreads();
   }
   const double* u1 = U1 + 2 * t * P1 + g;
   const double* u2 = U2 + g * P2 + t;
+  // left-over ranks 8RT .. 8RT+LO-1 of rows 8grp + 2t, 8grp + 2t + 1 (the rows
+  // of this lane's slice values): image 2, natural rank order
+  const double* ulo = U2 + 2 * t * P2 + 8 * RT;
 
   double racc = 0.0, xacc = 0.0;
   int j = 0;
@@ -360,6 +388,9 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
 #pragma unroll
       for (int rt = 0; rt < RT; ++rt) acc[h][rt][0] = acc[h][rt][1] = 0.0;
     double xs = 0.0;
+    double lp[2][LO > 0 ? LO : 1];
+#pragma unroll
+    for (int l = 0; l < (LO > 0 ? LO : 1); ++l) lp[0][l] = lp[1][l] = 0.0;
     const int dbg = a.karg1;  // profiling only: 16 skip phase 2, 32 skip phase 1
     // two row groups per step, written so consecutive DMMAs belong to
     // different accumulator chains: (grp, rt, x) for both groups, then
@@ -390,6 +421,47 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
         xs = fma(x0.y, x0.y, xs);
         xs = fma(x1.x, x1.x, xs);
         xs = fma(x1.y, x1.y, xs);
+        if constexpr (LO > 0) {
+          // left-over ranks on the FMA pipe: this lane's rows of column g
+          if constexpr (LO == 2) {  // ranks 8RT, 8RT+1 are one 16-byte load per row
+            const double2 a0 = *reinterpret_cast<const double2*>(ulo + (8 * grp) * P2);
+            const double2 a1 = *reinterpret_cast<const double2*>(ulo + (8 * grp + 1) * P2);
+            lp[0][0] = fma(x0.x, a0.x, lp[0][0]);
+            lp[0][1] = fma(x0.x, a0.y, lp[0][1]);
+            lp[0][0] = fma(x0.y, a1.x, lp[0][0]);
+            lp[0][1] = fma(x0.y, a1.y, lp[0][1]);
+            if (two) {
+              const double2 b0_ = *reinterpret_cast<const double2*>(ulo + (8 * grp + 8) * P2);
+              const double2 b1_ = *reinterpret_cast<const double2*>(ulo + (8 * grp + 9) * P2);
+              lp[1][0] = fma(x1.x, b0_.x, lp[1][0]);
+              lp[1][1] = fma(x1.x, b0_.y, lp[1][1]);
+              lp[1][0] = fma(x1.y, b1_.x, lp[1][0]);
+              lp[1][1] = fma(x1.y, b1_.y, lp[1][1]);
+            }
+          } else {
+#pragma unroll
+            for (int l = 0; l < LO; ++l) {
+              lp[0][l] = fma(x0.x, ulo[(8 * grp) * P2 + l], lp[0][l]);
+              lp[0][l] = fma(x0.y, ulo[(8 * grp + 1) * P2 + l], lp[0][l]);
+              if (two) {
+                lp[1][l] = fma(x1.x, ulo[(8 * grp + 8) * P2 + l], lp[1][l]);
+                lp[1][l] = fma(x1.y, ulo[(8 * grp + 9) * P2 + l], lp[1][l]);
+              }
+            }
+          }
+        }
+      }
+    }
+    double pl[LO > 0 ? LO : 1];
+    if constexpr (LO > 0) {
+      // sum over the four lanes (t) that share column g: every lane ends with
+      // the same bits (commutative pairings)
+#pragma unroll
+      for (int l = 0; l < LO; ++l) {
+        double v = lp[0][l] + lp[1][l];
+        v += __shfl_xor_sync(0xffffffffu, v, 1);
+        v += __shfl_xor_sync(0xffffffffu, v, 2);
+        pl[l] = v;
       }
     }
     double pa[RT][2];
@@ -406,6 +478,11 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
           const int rk = 8 * rt + 4 * i + t;
           if (rk < R) dst[rk] = pa[rt][i];
         }
+      if constexpr (LO > 0) {
+#pragma unroll
+        for (int l = 0; l < LO; ++l)
+          if (t == l) dst[8 * RT + l] = pl[l];
+      }
     }
     // ---- phase 2 + epilogue from registers
     double rs = 0.0;
@@ -430,6 +507,34 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
         for (int k = 0; k < KS; ++k) {
           dmma(c0, c1, pa[k >> 1][k & 1], bv0[k]);
           if (two) dmma(d0, d1, pa[k >> 1][k & 1], bv1[k]);
+        }
+        if constexpr (LO > 0) {
+          if constexpr (LO == 2) {
+            const double2 a0 = *reinterpret_cast<const double2*>(ulo + (8 * grp) * P2);
+            const double2 a1 = *reinterpret_cast<const double2*>(ulo + (8 * grp + 1) * P2);
+            c0 = fma(a0.x, pl[0], c0);
+            c0 = fma(a0.y, pl[1], c0);
+            c1 = fma(a1.x, pl[0], c1);
+            c1 = fma(a1.y, pl[1], c1);
+            if (two) {
+              const double2 b0_ = *reinterpret_cast<const double2*>(ulo + (8 * grp + 8) * P2);
+              const double2 b1_ = *reinterpret_cast<const double2*>(ulo + (8 * grp + 9) * P2);
+              d0 = fma(b0_.x, pl[0], d0);
+              d0 = fma(b0_.y, pl[1], d0);
+              d1 = fma(b1_.x, pl[0], d1);
+              d1 = fma(b1_.y, pl[1], d1);
+            }
+          } else {
+#pragma unroll
+            for (int l = 0; l < LO; ++l) {
+              c0 = fma(ulo[(8 * grp) * P2 + l], pl[l], c0);
+              c1 = fma(ulo[(8 * grp + 1) * P2 + l], pl[l], c1);
+              if (two) {
+                d0 = fma(ulo[(8 * grp + 8) * P2 + l], pl[l], d0);
+                d1 = fma(ulo[(8 * grp + 9) * P2 + l], pl[l], d1);
+              }
+            }
+          }
         }
         rs = fma(c0, c0, rs);
         rs = fma(c1, c1, rs);
@@ -465,7 +570,7 @@ __global__ void __launch_bounds__(32 * NW, 1) proj0_colsr_kernel(ProjArgs a) {
   }
 }
 
-template <int RT, int NW, int NG, bool HALF>
+template <int RT, int NW, int NG, bool HALF, int LO = 0>
 inline int launch_r(const ProjArgs& a, cudaStream_t st, int free_sms) {
   constexpr long long N = 8 * NG;
   const size_t smem =
@@ -473,7 +578,7 @@ inline int launch_r(const ProjArgs& a, cudaStream_t st, int free_sms) {
   if (smem > 227 * 1024) return -1;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(proj0_colsr_kernel<RT, NW, NG, HALF>,
+    if (cudaFuncSetAttribute(proj0_colsr_kernel<RT, NW, NG, HALF, LO>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
       return -1;
     attr = true;
@@ -484,8 +589,19 @@ inline int launch_r(const ProjArgs& a, cudaStream_t st, int free_sms) {
   const long long warps = (ntiles + per - 1) / per;
   int grid = (int)((warps + NW - 1) / NW);
   if (grid < 1) grid = 1;
-  proj0_colsr_kernel<RT, NW, NG, HALF><<<grid, 32 * NW, smem, st>>>(a);
+  proj0_colsr_kernel<RT, NW, NG, HALF, LO><<<grid, 32 * NW, smem, st>>>(a);
   return grid;
+}
+
+// one full DMMA rank tile + LO left-over ranks on the FMA pipe (R = 9..11)
+template <int NW, int NG>
+inline int launch_lo(const ProjArgs& a, cudaStream_t st, int free_sms, int lo) {
+  switch (lo) {
+    case 1: return launch_r<1, NW, NG, false, 1>(a, st, free_sms);
+    case 2: return launch_r<1, NW, NG, false, 2>(a, st, free_sms);
+    case 3: return launch_r<1, NW, NG, false, 3>(a, st, free_sms);
+  }
+  return -1;
 }
 
 template <int RT, int NW, int NG>
@@ -535,6 +651,11 @@ inline int launch(const ProjArgs& a, cudaStream_t st) {
   }();
   const int RT = (a.R + 7) / 8;
   int g = -1;
+  if (const int lo = cols_lo(a.v.n, a.R)) {
+    if (a.v.n == 200) g = launch_lo<12, 25>(a, st, free_sms, lo);
+    if (a.v.n == 256) g = launch_lo<8, 32>(a, st, free_sms, lo);
+    return g;  // the prebuilt images follow cols_rt: no other kernel reads them
+  }
   // A/B variants (TSG_PROJ0_COLS): 1 = 6 warps x 2 buffers, 2 = 8 warps x 1,
   // 3 = 12 warps x 1, 4 = 4 warps x 3; each falls back to the 4 x 2 shape
   // when its shared memory does not fit
