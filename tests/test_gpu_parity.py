@@ -48,6 +48,59 @@ def test_async_mode_matches_sync(golden):
     np.testing.assert_array_equal(a.left, b.left)
 
 
+@pytest.mark.parametrize("device_slices", [False, True])
+def test_async_consecutive_slow_paths_match_sync(oracle, device_slices):
+    """The pipelined engine defers two slices (projections of t+1, t+2 are
+    enqueued before the decision of t is acted on). Here several consecutive
+    slices take the slow path — basis growth on most slices of the config-4
+    generator, plus zero slices — so the younger deferred slices are
+    re-projected repeatedly. Results are bitwise those of the synchronous
+    engine and match the CPU checker; with device inputs the caller's tensors
+    stay untouched."""
+    import torch
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.scaled(dg.CONFIGS["c4"], (48, 48, 48, 16), n_slices=19, n_init=10, name="c4_stress")
+    case = cases.config_case(cfg)
+    slices = [y.copy() for y in case.slices]
+    slices.insert(2, np.zeros_like(slices[0]))   # two consecutive zero slices between growths
+    slices.insert(2, np.zeros_like(slices[0]))
+    case = cases.StreamCase(case.name, case.init_flat, case.init_dims, slices, case.tau)
+
+    def run(asynchronous):
+        st = S.StreamingState(asynchronous=asynchronous)
+        st.init_flat(case.init_flat, case.init_dims, case.tau)
+        keep = []
+        for y in case.slices:
+            if device_slices:
+                ty = torch.from_numpy(y).cuda()
+                keep.append((ty, ty.clone()))
+                st.stream_update(ty)
+            else:
+                st.stream_update(y)
+        st.synchronize()
+        for ty, t0 in keep:
+            assert torch.equal(ty, t0)
+        return st
+
+    sa, ss = run(True), run(False)
+    a, b = sa.export(), ss.export()
+    assert a.core_dims == b.core_dims and a.n_d == b.n_d
+    np.testing.assert_array_equal(a.core, b.core)
+    np.testing.assert_array_equal(a.left, b.left)
+    np.testing.assert_array_equal(a.sigma, b.sigma)
+    for fa, fb in zip(a.factors, b.factors):
+        np.testing.assert_array_equal(fa, fb)
+    assert [m["expanded_mask"] for m in sa.metrics()] == [m["expanded_mask"] for m in ss.metrics()]
+    assert sum(1 for m in sa.metrics() if m["expanded_mask"]) >= 4
+    ho = _oracle_run(oracle, case)
+    so = ho.export()
+    mc = P.compare_metrics(P.metrics_arrays(sa.metrics(), a.order),
+                           P.metrics_arrays(ho.metrics(), so.order), so.total_input_sq)
+    sc = P.compare_states(a, so)
+    print("stress", mc, sc)
+    P.assert_parity(mc, sc, resid_tol=5e-8)
+
+
 def test_blocks_vs_golden(golden):
     g = golden("blocks")
     b = cases.blocks_inputs()
