@@ -1513,18 +1513,24 @@ struct tsg_stream {
     ex->send = sh_send;
     ex->recv = sh_recv;
   }
-  void shard_done(tsg_exchange* ex) {
+  // `in_flight`: the slice took the fast path and its insertion is only
+  // enqueued — the call returns without a synchronisation, the record
+  // arrives through the mapped ring (published by a later slice's decision
+  // kernel) and the host work of the next slice overlaps this insertion.
+  void shard_done(tsg_exchange* ex, bool in_flight = false) {
     sh_phase = 0;
-    // the slice's record arrives through the mapped ring (no stream sync and
-    // no control-block copy on the way out)
-    drain(true);
-    if (have_last_ctrl && pending.empty()) {
-      *ctrl_h = last_ctrl;
-      ck(cudaGetLastError(), "kernel");
+    if (in_flight) {
+      drain(false);
     } else {
-      pull_ctrl();
+      drain(true);
+      if (have_last_ctrl && pending.empty()) {
+        *ctrl_h = last_ctrl;
+        ck(cudaGetLastError(), "kernel");
+      } else {
+        pull_ctrl();
+      }
+      r_exact = ctrl_h->r;
     }
-    r_exact = ctrl_h->r;
     ex->pending = 0;
     ex->op = TSG_XCHG_ALLGATHER;
     ex->count = 0;
@@ -1547,7 +1553,7 @@ struct tsg_stream {
     if (!initialized) fail(TSG_EINVAL, "stream_update: state not initialised");
     if (shard_world == 0) fail(TSG_EINVAL, "tsg_shard_begin: call tsg_shard_setup first");
     if (sh_phase != 0) fail(TSG_EINVAL, "tsg_shard_begin: the previous slice's exchange is pending");
-    if (!deferred.empty() || !pending.empty()) flush();  // a preceding async tsg_update
+    if (!deferred.empty()) flush();  // a preceding async tsg_update
     sh_t0 = std::chrono::steady_clock::now();
     const long long le = slice_elems / N[shard_mode] * shard_n[shard_rank];
     const bool misaligned = (reinterpret_cast<uintptr_t>(slab) & 15) != 0;
@@ -1690,9 +1696,13 @@ struct tsg_stream {
     }
     SliceCtl sc;
     if (m0 == 0) {
-      // the decision comes back through the mapped slot (a spin, no copy call)
+      // the decision comes back through the mapped slot (a spin, no copy
+      // call); the same kernel publishes the records of completed insertions
       da.host_slot = hslot_d;
       da.seq_counter = seq_dev;
+      da.ring_dev = ring_dev;
+      da.ring_host = ring_d;
+      da.ring_pub = ring_pub;
       ++seq_expect[0];
       launch_decide(da, st);
       sc = wait_slot(0);
@@ -1709,6 +1719,8 @@ struct tsg_stream {
     } else if (sc.expand_mode < 0) {
       if (m0 == 0) {
         enqueue_isvd(cur, 0, 0, st, true, sh_t0);
+        shard_done(ex, /*in_flight=*/true);
+        return;
       } else {
         launch_commit_modes(ctrl, slots, m0, d - 1, with_total, st);
         pull_ctrl();
