@@ -266,6 +266,7 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
   const bool use_wide = wide != nullptr && m <= secular::kWide;
   int sweep = 0;
   if (use_wide) {
+    TSG_CLK(4);
     if (threadIdx.x < 32) {
       const int lane = threadIdx.x;
       secular::ScratchWide S = secular::scratch_wide(wide);
@@ -282,6 +283,7 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
     }
     __syncthreads();
     sweep = sh_iters;
+    TSG_CLK(5);
   } else {
   double acc = 0.0;
   for (int idx = threadIdx.x; idx < m * m; idx += blockDim.x) {
@@ -438,6 +440,7 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
   }  // !use_wide (the secular solver returns sorted, signed eigenpairs)
   if (threadIdx.x == 0) sh_rank = inner_truncate(io, lam, m, sweep);
   __syncthreads();
+  if (use_wide) TSG_CLK(6);
   const int rank = sh_rank;
   double* U = io.inner + L.U;
   for (int j = threadIdx.x; j < rank; j += blockDim.x) io.sigma_new[j] = sqrt(lam[j]);
@@ -477,6 +480,7 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
       }
       __syncthreads();
     }
+    TSG_CLK(7);
     for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) U[idx] = sU[idx];
     double* M = io.inner + L.M;
     double* w = io.inner + L.w;
@@ -488,6 +492,7 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
     }
     for (int j = threadIdx.x; j < rank; j += blockDim.x) w[j] = sU[r + j * rows];
     __syncthreads();
+    TSG_CLK(2);
     return;
   }
   for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) {
@@ -921,6 +926,22 @@ __global__ void __launch_bounds__(1024) pgram_kernel(const Ctrl* ctrl, const dou
   }
 }
 
+// out[j] = sum over the nblk per-block partials of column j (j < r): a warp per
+// column, lanes stride the blocks so every load is in flight at once, fixed
+// shuffle tree. Pass 2, pass 3 and the inner kernel all sum in this order, so
+// they see the same bits. (One thread per column used to walk the ~180
+// partials one dependent L2 round trip at a time.)
+__device__ __forceinline__ void column_sums(const double* __restrict__ part, int nblk, int capr,
+                                            int r, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int j = wid; j < r; j += nw) {
+    double s = 0.0;
+    for (int b = lane; b < nblk; b += 32) s += part[(long long)b * (capr + 1) + j];
+    s = warp_sum(s);
+    if (lane == 0) out[j] = s;
+  }
+}
+
 __global__ void __launch_bounds__(256) isvd_pass1_kernel(const Ctrl* ctrl, const double* __restrict__ q,
                                                          const double* __restrict__ b, long long n,
                                                          long long rows_per, int capr,
@@ -954,11 +975,7 @@ __global__ void __launch_bounds__(256) isvd_pass2_kernel(const Ctrl* ctrl, const
                                                          double* __restrict__ part2) {
   extern __shared__ double ps[];
   const int r = ctrl->r;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) {
-    double s = 0.0;
-    for (int bb = 0; bb < nblk; ++bb) s += part1[(long long)bb * (capr + 1) + j];
-    ps[j] = s;
-  }
+  column_sums(part1, nblk, capr, r, ps);
   __syncthreads();
   const long long i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
   for (long long i = i0 + threadIdx.x; i < i1; i += blockDim.x) {
@@ -988,11 +1005,7 @@ __global__ void __launch_bounds__(256) isvd_pass3_kernel(const Ctrl* ctrl, const
   extern __shared__ double ps[];
   __shared__ double red[32];
   const int r = ctrl->r;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) {
-    double s = 0.0;
-    for (int bb = 0; bb < nblk; ++bb) s += part2[(long long)bb * (capr + 1) + j];
-    ps[j] = s;
-  }
+  column_sums(part2, nblk, capr, r, ps);
   __syncthreads();
   const long long i0 = blockIdx.x * rows_per, i1 = min(n, i0 + rows_per);
   double acc = 0.0;
@@ -1032,11 +1045,23 @@ __global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
   Ctrl* c = a.ctrl;
   const int r = c->r;
   double* p = a.inner + L.p;
-  for (int j = threadIdx.x; j < r; j += blockDim.x) {
-    double s1 = 0.0, s2 = 0.0;
-    for (int b = 0; b < a.nblk; ++b) s1 += a.part1[(long long)b * (a.capr + 1) + j];
-    for (int b = 0; b < a.nblk; ++b) s2 += a.part2[(long long)b * (a.capr + 1) + j];
-    p[j] = s1 + s2;
+  TSG_CLK(0);
+  {
+    // p_j = sum_b part1[b][j] + sum_b part2[b][j]: a warp per column, lanes
+    // stride the blocks (all loads in flight), fixed shuffle tree. (One
+    // thread per column walked the ~180 partials of each array one dependent
+    // L2 round trip at a time: ~55 us of the 170 us inner kernel.)
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = wid; j < r; j += nw) {
+      double s1 = 0.0, s2 = 0.0;
+      for (int b = lane; b < a.nblk; b += 32) {
+        s1 += a.part1[(long long)b * (a.capr + 1) + j];
+        s2 += a.part2[(long long)b * (a.capr + 1) + j];
+      }
+      s1 = warp_sum(s1);
+      s2 = warp_sum(s2);
+      if (lane == 0) p[j] = s1 + s2;
+    }
   }
   double bs = 0.0, es = 0.0;
   for (int b = threadIdx.x; b < a.nblk; b += blockDim.x) {
@@ -1052,6 +1077,7 @@ __global__ void __launch_bounds__(512) isvd_inner_kernel(InnerArgs a) {
     c->e_sq = es;
   }
   __syncthreads();
+  TSG_CLK(1);
   InnerIO io;
   io.ctrl = c;
   io.r = r;

@@ -391,21 +391,22 @@ __global__ void __launch_bounds__(128) tri_backtransform_kernel(int n, double* w
     double dot = 0.0;
     double vloc[8];
     int c = 0;
-    for (int i = k + 1 + tid; i < n; i += 128) {
-      const double vi = vk[i];
+    // entries are owned by a FIXED thread (i mod 128 == tid) in every step:
+    // a thread only ever reads and writes its own z[i], so the barriers inside
+    // block_sum are the only ones needed (v_k is zero for i <= k)
+    for (int i = tid; i < n; i += 128) {
+      const double vi = i > k ? vk[i] : 0.0;
       if (c < 8) vloc[c] = vi;
       ++c;
       dot += vi * z[i];
     }
     dot = block_sum(dot, red) * b;
     c = 0;
-    for (int i = k + 1 + tid; i < n; i += 128) {
-      const double vi = c < 8 ? vloc[c] : vk[i];
+    for (int i = tid; i < n; i += 128) {
+      const double vi = c < 8 ? vloc[c] : (i > k ? vk[i] : 0.0);
       ++c;
       z[i] -= dot * vi;
     }
-    // each thread touches only its own entries of z between the barriers
-    // inside block_sum, so no extra barrier is needed here
   }
   __syncthreads();
   // sign rule: the entry of largest magnitude (first index on ties) is positive
