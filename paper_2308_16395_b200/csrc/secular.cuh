@@ -418,6 +418,7 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
     sh_rot = rotated;
   }
   __syncwarp();
+  SEC_CLK(10);
   const int K = sh_K;
   int iters = 0;
   for (int j = lane; j < K; j += 32) {
@@ -430,6 +431,7 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) iters = max(iters, __shfl_xor_sync(FULL, iters, off));
   __syncwarp();
+  SEC_CLK(11);
   // Loewner z-hat
   for (int i = lane; i < K; i += 32) {
     const double di = S.dK[i];
@@ -476,6 +478,7 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
     S.perm[rk] = q;
   }
   __syncwarp();
+  SEC_CLK(12);
   // eigenvector columns, sign rule, clamp
   for (int col = lane; col < m; col += 32) {
     const int src = S.perm[col];
