@@ -267,22 +267,20 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
   int sweep = 0;
   if (use_wide) {
     TSG_CLK(4);
-    if (threadIdx.x < 32) {
-      const int lane = threadIdx.x;
+    {
       secular::ScratchWide S = secular::scratch_wide(wide);
       double* d_in = wide + secular::ScratchWide::doubles();
       double* z_in = d_in + secular::kWide;
-      for (int i = lane; i < m; i += 32) {
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
         const double sg = i < r ? io.sigma[i] : 0.0;
         d_in[i] = sg * sg;
         z_in[i] = i < r ? io.p[i] : io.k;
       }
-      __syncwarp();
-      const int it = secular::eig_rank_one_wide(m, d_in, z_in, S, io.inner + L.lam, io.inner + L.W);
-      if (lane == 0) sh_iters = it;
+      __syncthreads();
+      // block-wide: one thread per root / coordinate / column
+      sweep = secular::eig_rank_one_wide(m, d_in, z_in, S, io.inner + L.lam, io.inner + L.W);
     }
-    __syncthreads();
-    sweep = sh_iters;
+    (void)sh_iters;
     TSG_CLK(5);
   } else {
   double acc = 0.0;
@@ -448,35 +446,46 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
     // U = S' W / sigma and its MGS pass in shared memory (the secular
     // scratch is free now), a warp per column with lanes over the rows
     double* sU = wide;  // rows x rank, ld rows (<= 65 x 64)
-    for (int idx = threadIdx.x; idx < rows * rank; idx += blockDim.x) {
-      const int i = idx % rows, j = idx / rows;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int idx = threadIdx.x; idx < r * rank; idx += blockDim.x) {
+      const int i = idx % r, j = idx / r;
+      // rows i < r of S' are diag(s)
+      sU[i + j * rows] = io.sigma[i] * W[i + j * m] * (1.0 / sqrt(lam[j]));
+    }
+    // last row [p^T k] W: a warp per column, lanes over the m terms (all loads
+    // in flight), fixed tree
+    for (int j = wid; j < rank; j += nw) {
       double s = 0.0;
-      if (i < r) {
-        s = io.sigma[i] * W[i + j * m];                   // rows i < r of S' are diag(s)
-      } else {
-        for (int l = 0; l < m; ++l) s += Sp(io, r, l) * W[l + j * m];
-      }
-      sU[i + j * rows] = s * (1.0 / sqrt(lam[j]));
+      for (int l = lane; l < m; l += 32) s += Sp(io, r, l) * W[l + j * m];
+      s = warp_sum(s);
+      if (lane == 0) sU[r + j * rows] = s * (1.0 / sqrt(lam[j]));
     }
     __syncthreads();
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    TSG_CLK(17);
+    auto normalize = [&](double* u) {  // one warp
+      double ss = 0.0;
+      for (int l = lane; l < rows; l += 32) ss += u[l] * u[l];
+      ss = warp_sum(ss);
+      const double nrm = sqrt(ss);
+      __syncwarp();
+      if (nrm > 0.0)
+        for (int l = lane; l < rows; l += 32) u[l] /= nrm;
+      __syncwarp();
+    };
+    if (wid == 0 && rank > 0) normalize(sU);
+    __syncthreads();
+    // one barrier per column: the warp that updates column i + 1 normalises it
+    // right away (the same operations in the same order as a separate pass)
     for (int i = 0; i < rank; ++i) {
-      double* ui = sU + i * rows;
-      if (wid == 0) {
-        double ss = 0.0;
-        for (int l = lane; l < rows; l += 32) ss += ui[l] * ui[l];
-        ss = warp_sum(ss);
-        const double nrm = sqrt(ss);
-        if (nrm > 0.0)
-          for (int l = lane; l < rows; l += 32) ui[l] /= nrm;
-      }
-      __syncthreads();
+      const double* ui = sU + i * rows;
       for (int j = i + 1 + wid; j < rank; j += nw) {
         double* uj = sU + j * rows;
         double dot = 0.0;
         for (int l = lane; l < rows; l += 32) dot += ui[l] * uj[l];
         dot = warp_sum(dot);
         for (int l = lane; l < rows; l += 32) uj[l] -= dot * ui[l];
+        __syncwarp();
+        if (j == i + 1) normalize(uj);
       }
       __syncthreads();
     }

@@ -358,50 +358,80 @@ __device__ inline ScratchWide scratch_wide(double* base) {
 
 // d_in (m, descending, >= 0), z_in (m): eigenvalues of diag(d) + z z^T into
 // lam (descending, clamped >= 0), eigenvectors into W (m x m column-major,
-// ld m) with the reference's sign rule. Called by one full warp.
+// ld m) with the reference's sign rule. Called by EVERY thread of the CTA
+// (block barriers inside): one thread per root / coordinate / column, so the
+// 33..64-column problem takes about as long as one root instead of two per
+// lane of a single warp; the sequential Givens deflation of close poles runs
+// only when a close pair exists (rare), after a parallel scan.
 __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const double* z_in, ScratchWide S,
                                  double* lam, double* W) {
-  const int lane = threadIdx.x & 31;
-  __shared__ int sh_K, sh_rot;
-  __shared__ double sh_wsum;
-  for (int i = lane; i < m * m; i += 32) {
-    const int a = i % m, b = i / m;
-    S.sQ[a * PW + b] = (a == b) ? 1.0 : 0.0;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  __shared__ int sh_K, sh_rot, sh_close, sh_iters;
+  __shared__ double sh_wsum, sh_zn2;
+  for (int i = tid; i < m * PW; i += nt) {
+    const int a_ = i / PW, b_ = i - a_ * PW;
+    S.sQ[i] = (a_ == b_) ? 1.0 : 0.0;
   }
-  for (int i = lane; i < m; i += 32) {
+  for (int i = tid; i < m; i += nt) {
     S.dwork[i] = d_in[i];
     S.zK[i] = z_in[i];
   }
-  __syncwarp();
-  if (lane == 0) {
+  if (tid == 0) {
+    sh_close = 0;
+    sh_iters = 0;
+  }
+  __syncthreads();
+  if (tid < 32) {  // ||z||^2 in coordinate order per lane, fixed tree
     double zn2 = 0.0;
-    for (int i = 0; i < m; ++i) zn2 += S.zK[i] * S.zK[i];
-    const double zn = sqrt(zn2);
-    const double tol = 8.0 * DBL_EPSILON * (S.dwork[0] + zn2);
-    for (int i = 0; i < m; ++i) S.flag[i] = (fabs(S.zK[i]) * zn <= tol) ? 1 : 0;
-    int prev = -1, rotated = 0;
-    for (int i = 0; i < m; ++i) {
-      if (S.flag[i]) continue;
-      if (prev >= 0 && fabs(S.dwork[prev] - S.dwork[i]) * fabs(S.zK[prev] * S.zK[i]) <=
-                           tol * (S.zK[prev] * S.zK[prev] + S.zK[i] * S.zK[i])) {
-        const double zp = S.zK[prev], zi = S.zK[i];
-        const double rr = hypot(zp, zi);
-        const double c = zp / rr, sn = zi / rr;
-        rotated = 1;
-        const double dp = S.dwork[prev], di = S.dwork[i];
-        S.dwork[prev] = c * c * dp + sn * sn * di;
-        S.dwork[i] = sn * sn * dp + c * c * di;
-        S.zK[prev] = rr;
-        S.zK[i] = 0.0;
-        for (int a = 0; a < m; ++a) {
-          const double qp = S.sQ[a * PW + prev], qi = S.sQ[a * PW + i];
-          S.sQ[a * PW + prev] = c * qp + sn * qi;
-          S.sQ[a * PW + i] = -sn * qp + c * qi;
+    for (int i = tid; i < m; i += 32) zn2 += S.zK[i] * S.zK[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) zn2 += __shfl_xor_sync(FULL, zn2, off);
+    if (tid == 0) sh_zn2 = zn2;
+  }
+  __syncthreads();
+  const double zn2 = sh_zn2;
+  const double tol = 8.0 * DBL_EPSILON * (S.dwork[0] + zn2);
+  const double zn = sqrt(zn2);
+  for (int i = tid; i < m; i += nt) S.flag[i] = (fabs(S.zK[i]) * zn <= tol) ? 1 : 0;
+  __syncthreads();
+  // any close pair among consecutive kept coordinates?
+  for (int i = tid; i < m; i += nt) {
+    if (S.flag[i]) continue;
+    int prev = i - 1;
+    while (prev >= 0 && S.flag[prev]) --prev;
+    if (prev >= 0 && fabs(S.dwork[prev] - S.dwork[i]) * fabs(S.zK[prev] * S.zK[i]) <=
+                         tol * (S.zK[prev] * S.zK[prev] + S.zK[i] * S.zK[i]))
+      sh_close = 1;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int rotated = 0;
+    if (sh_close) {
+      // close poles: rotate the later coordinate's weight into the earlier one
+      int prev = -1;
+      for (int i = 0; i < m; ++i) {
+        if (S.flag[i]) continue;
+        if (prev >= 0 && fabs(S.dwork[prev] - S.dwork[i]) * fabs(S.zK[prev] * S.zK[i]) <=
+                             tol * (S.zK[prev] * S.zK[prev] + S.zK[i] * S.zK[i])) {
+          const double zp = S.zK[prev], zi = S.zK[i];
+          const double rr = hypot(zp, zi);
+          const double c = zp / rr, sn = zi / rr;
+          rotated = 1;
+          const double dp = S.dwork[prev], di = S.dwork[i];
+          S.dwork[prev] = c * c * dp + sn * sn * di;
+          S.dwork[i] = sn * sn * dp + c * c * di;
+          S.zK[prev] = rr;
+          S.zK[i] = 0.0;
+          for (int a_ = 0; a_ < m; ++a_) {
+            const double qp = S.sQ[a_ * PW + prev], qi = S.sQ[a_ * PW + i];
+            S.sQ[a_ * PW + prev] = c * qp + sn * qi;
+            S.sQ[a_ * PW + i] = -sn * qp + c * qi;
+          }
+          S.flag[i] = 1;
+          continue;
         }
-        S.flag[i] = 1;
-        continue;
+        prev = i;
       }
-      prev = i;
     }
     int K = 0;
     double wsum = 0.0;
@@ -417,23 +447,21 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
     sh_wsum = wsum;
     sh_rot = rotated;
   }
-  __syncwarp();
+  __syncthreads();
   SEC_CLK(10);
   const int K = sh_K;
-  int iters = 0;
-  for (int j = lane; j < K; j += 32) {
+  for (int j = tid; j < K; j += nt) {
     int o;
     double tau;
-    iters = max(iters, solve_root(S.dK, S.wK, K, sh_wsum, j, o, tau));
+    const int it = solve_root(S.dK, S.wK, K, sh_wsum, j, o, tau);
     S.ls[j] = S.dK[o];
     S.lt[j] = tau;
+    atomicMax(&sh_iters, it);
   }
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) iters = max(iters, __shfl_xor_sync(FULL, iters, off));
-  __syncwarp();
+  __syncthreads();
   SEC_CLK(11);
   // Loewner z-hat
-  for (int i = lane; i < K; i += 32) {
+  for (int i = tid; i < K; i += nt) {
     const double di = S.dK[i];
     double prod = (S.ls[i] - di) + S.lt[i];
     for (int j = 0; j < K; ++j) {
@@ -445,19 +473,18 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
     const double mag = sqrt(fabs(prod));
     S.zh[i] = (zi < 0.0) ? -mag : mag;
   }
-  __syncwarp();
   // all eigenvalues: non-deflated roots, then deflated poles in coordinate order
-  for (int q = lane; q < m; q += 32) {
+  for (int q = tid; q < m; q += nt) {
     double lv;
     if (q < K) {
       lv = S.ls[q] + S.lt[q];
       S.kind[q] = q;
     } else {
       int cnt = 0, coord = 0;
-      for (int a = 0; a < m; ++a)
-        if (S.flag[a]) {
+      for (int a_ = 0; a_ < m; ++a_)
+        if (S.flag[a_]) {
           if (cnt == q - K) {
-            coord = a;
+            coord = a_;
             break;
           }
           ++cnt;
@@ -467,8 +494,8 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
     }
     S.lamall[q] = lv;
   }
-  __syncwarp();
-  for (int q = lane; q < m; q += 32) {
+  __syncthreads();
+  for (int q = tid; q < m; q += nt) {
     const double li = S.lamall[q];
     int rk = 0;
     for (int j = 0; j < m; ++j) {
@@ -477,13 +504,13 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
     }
     S.perm[rk] = q;
   }
-  __syncwarp();
+  __syncthreads();
   SEC_CLK(12);
   // eigenvector columns, sign rule, clamp
-  for (int col = lane; col < m; col += 32) {
+  for (int col = tid; col < m; col += nt) {
     const int src = S.perm[col];
     const int kind = S.kind[src];
-    for (int a = 0; a < m; ++a) S.sW[a * PW + col] = 0.0;
+    for (int a_ = 0; a_ < m; ++a_) S.sW[a_ * PW + col] = 0.0;
     if (kind < kWide) {
       const int j = kind;
       double nrm2 = 0.0;
@@ -499,32 +526,32 @@ __device__ __noinline__ int eig_rank_one_wide(int m, const double* d_in, const d
         for (int i = 0; i < K; ++i) {
           const double c = S.zh[i] * rcp((S.dK[i] - S.ls[j]) - S.lt[j]) * inv;
           const int coord = S.idx[i];
-          for (int a = 0; a < m; ++a) S.sW[a * PW + col] += S.sQ[a * PW + coord] * c;
+          for (int a_ = 0; a_ < m; ++a_) S.sW[a_ * PW + col] += S.sQ[a_ * PW + coord] * c;
         }
       }
     } else {
       const int coord = kind - kWide;
-      for (int a = 0; a < m; ++a) S.sW[a * PW + col] = S.sQ[a * PW + coord];
+      for (int a_ = 0; a_ < m; ++a_) S.sW[a_ * PW + col] = S.sQ[a_ * PW + coord];
     }
     int arg = 0;
     double best = fabs(S.sW[col]);
-    for (int a = 1; a < m; ++a) {
-      const double av = fabs(S.sW[a * PW + col]);
+    for (int a_ = 1; a_ < m; ++a_) {
+      const double av = fabs(S.sW[a_ * PW + col]);
       if (av > best) {
         best = av;
-        arg = a;
+        arg = a_;
       }
     }
     const bool flip = S.sW[arg * PW + col] < 0.0;
-    for (int a = 0; a < m; ++a) {
-      const double v = flip ? -S.sW[a * PW + col] : S.sW[a * PW + col];
-      W[a + col * m] = v;
+    for (int a_ = 0; a_ < m; ++a_) {
+      const double v = flip ? -S.sW[a_ * PW + col] : S.sW[a_ * PW + col];
+      W[a_ + col * m] = v;
     }
     const double lv = S.lamall[src];
     lam[col] = lv < 0.0 ? 0.0 : lv;
   }
-  __syncwarp();
-  return iters;
+  __syncthreads();
+  return sh_iters;
 }
 
 // Register-resident variant for m <= KM: the deflation scan, root solve,

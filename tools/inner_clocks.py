@@ -20,6 +20,6 @@ L.tsg_debug_isvd_clocks(c.ctypes.data_as(ctypes.c_void_p))
 f = lambda a, b: f"{(c[a] - c[b]) / 1965:7.1f} us"
 print("ranks", st.query()["core_dims"])
 print("partial sums", f(1, 0), "| pre", f(4, 1), "| secular (wide)", f(5, 4), "| truncate", f(6, 5),
-      "| U + MGS", f(7, 6), "| M, w, stores", f(2, 7), "| total", f(2, 0))
+      "| U fill", f(17, 6), "| MGS", f(7, 17), "| M, w, stores", f(2, 7), "| total", f(2, 0))
 print("wide secular: prologue + deflation", f(10, 4), "| roots", f(11, 10), "| z-hat, all eigenvalues, sort", f(12, 11),
       "| vectors", f(5, 12))
