@@ -418,6 +418,13 @@ struct tsg_stream {
     peak_bytes = std::max(peak_bytes, cur_bytes);
     return static_cast<double*>(p);
   }
+  // State buffers (Q, core, ...) are read up to a rank hint past the columns
+  // ever written: pooled memory is not zero, so they start cleared.
+  double* dalloc_zero(long long n_doubles) {
+    double* p = dalloc(n_doubles);
+    ck(cudaMemsetAsync(p, 0, sizeof(double) * (size_t)(n_doubles > 0 ? n_doubles : 1), st), "memset");
+    return p;
+  }
   void dfree(void* p) {
     if (!p) return;
     for (size_t i = 0; i < allocs.size(); ++i)
@@ -555,10 +562,10 @@ struct tsg_stream {
     // Q / core hold n x capr; left holds cap_rows x capr; sigma capr
     const long long n = n_rows();
     sync();
-    double* nq = dalloc(n * new_capr);
-    double* nc = dalloc(n * new_capr);
-    double* nq2 = dalloc(n * new_capr);
-    double* nc2 = dalloc(n * new_capr);
+    double* nq = dalloc_zero(n * new_capr);
+    double* nc = dalloc_zero(n * new_capr);
+    double* nq2 = dalloc_zero(n * new_capr);
+    double* nc2 = dalloc_zero(n * new_capr);
     ck(cudaMemcpyAsync(nq, Q, sizeof(double) * n * capr, cudaMemcpyDeviceToDevice, st), "grow");
     ck(cudaMemcpyAsync(nc, core, sizeof(double) * n * capr, cudaMemcpyDeviceToDevice, st), "grow");
     double* nl = dalloc(cap_rows * new_capr);
@@ -894,12 +901,12 @@ struct tsg_stream {
     // re-allocated with room for further growth.
     const bool in_spare = new_qcap <= qcap;
     const long long alloc_qcap = in_spare ? qcap : 2 * new_qcap;
-    double* nq = in_spare ? Q2 : dalloc(alloc_qcap);
-    double* nc = in_spare ? core2 : dalloc(alloc_qcap);
+    double* nq = in_spare ? Q2 : dalloc_zero(alloc_qcap);
+    double* nc = in_spare ? core2 : dalloc_zero(alloc_qcap);
     launch_pad(Q, cv, g, nq, st);
     launch_pad(core, cv, g, nc, st);
-    double* nq2 = in_spare ? Q : dalloc(alloc_qcap);
-    double* nc2 = in_spare ? core : dalloc(alloc_qcap);
+    double* nq2 = in_spare ? Q : dalloc_zero(alloc_qcap);
+    double* nc2 = in_spare ? core : dalloc_zero(alloc_qcap);
     // ledger (streaming.cpp:150)
     double* dd = dalloc(1);
     ck(cudaMemcpyAsync(dd, &s.disc, 8, cudaMemcpyHostToDevice, st), "disc");
@@ -1013,7 +1020,18 @@ struct tsg_stream {
     // warm-up. The pipelined engine therefore rounds it up to the steady
     // bound r + kNP + 1 (arithmetic is RMAX-invariant, see DESIGN).
     int r_key = r_ub;
-    if (s_ == si && (flags & TSG_ASYNC)) r_key = std::max(r_ub, r_exact + kNP + 1);
+    if (s_ == si && (flags & TSG_ASYNC)) {
+      r_key = std::max(r_ub, r_exact + kNP + 1);
+      // ... and up to the next template bound, so that a streaming rank that
+      // creeps up one by one (config 5: 8 -> 36) re-captures the insertion
+      // graphs at ~10 bounds instead of at every rank
+      static const int bounds[] = {8, 12, 14, 16, 20, 24, 31, 39, 47, 63, 95, 127};
+      for (int bnd : bounds)
+        if (r_key <= bnd) {
+          r_key = bnd;
+          break;
+        }
+    }
     B.r_hint = std::min(r_key + rpad, capr - 1);
     B.commit_modes = commit ? d - 1 : 0;  // ledger commit fused into the insertion
     for (int k = 0; k + 1 < d; ++k) B.spatial_ranks[k] = R[k];
@@ -1861,10 +1879,10 @@ struct tsg_stream {
     if (cfg_capr > 0) capr = std::max<int>(capr, (int)cfg_capr);
     cap_rows = std::max<long long>(cfg_rows > 0 ? cfg_rows : 0, std::max(256LL, 2 * n_d));
     qcap = n * capr;
-    Q = dalloc(qcap);
-    Q2 = dalloc(qcap);
-    core = dalloc(qcap);
-    core2 = dalloc(qcap);
+    Q = dalloc_zero(qcap);
+    Q2 = dalloc_zero(qcap);
+    core = dalloc_zero(qcap);
+    core2 = dalloc_zero(qcap);
     sigma = dalloc(capr + 1);
     sigma2 = dalloc(capr + 1);
     left = dalloc(cap_rows * capr);
@@ -2096,7 +2114,7 @@ struct tsg_stream {
     capr = std::max(16, (2 * r + 8 + 7) / 8 * 8);
     cap_rows = std::max(256LL, 2 * n_d);
     qcap = n * capr;
-    Q = dalloc(qcap); Q2 = dalloc(qcap); core = dalloc(qcap); core2 = dalloc(qcap);
+    Q = dalloc_zero(qcap); Q2 = dalloc_zero(qcap); core = dalloc_zero(qcap); core2 = dalloc_zero(qcap);
     sigma = dalloc(capr + 1); sigma2 = dalloc(capr + 1);
     left = dalloc(cap_rows * capr); left2 = dalloc(cap_rows * capr);
     pgram = dalloc((long long)capr * capr);
