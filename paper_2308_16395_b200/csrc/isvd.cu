@@ -253,7 +253,7 @@ __device__ void inner_solve_warp(const InnerIO& io, double* sG, double* sU) {
 constexpr int kWideScratch = secular::ScratchWide::doubles() + 2 * secular::kWide;
 __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, double* wide = nullptr) {
   __shared__ double red[32];
-  __shared__ int sh_rank, sh_iters;
+  __shared__ int sh_rank;
   struct RotL {
     double c, s, t;
     int p, q;
@@ -280,7 +280,6 @@ __device__ void inner_solve_block(const InnerIO& io, double* G, double* V, doubl
       // block-wide: one thread per root / coordinate / column
       sweep = secular::eig_rank_one_wide(m, d_in, z_in, S, io.inner + L.lam, io.inner + L.W);
     }
-    (void)sh_iters;
     TSG_CLK(5);
   } else {
   double acc = 0.0;
