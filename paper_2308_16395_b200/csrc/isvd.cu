@@ -861,31 +861,30 @@ __global__ void __launch_bounds__(512, 1) isvd_fused_kernel(IsvdBufs B) {
 // row-major factor with one dependent L2 round trip per row (390 us at
 // n_d = 400, r = 36; ~15 us tiled).
 constexpr int kPgTile = 32;
-__global__ void __launch_bounds__(1024) pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left,
-                                                      int capr, double* pg) {
+constexpr int kPgThreads = 256;  // a light CTA: it must fit beside a persistent mode-0 CTA
+constexpr int kPgPairs = 8;      // (l, j) pairs per thread: r^2 <= 2048 (r <= 45)
+__global__ void __launch_bounds__(kPgThreads) pgram_kernel(const Ctrl* ctrl, const double* __restrict__ left,
+                                                            int capr, double* pg) {
   extern __shared__ double tile[];  // 2 x kPgTile x r
   const long long n_d = ctrl->n_d;
   const int r = ctrl->r;
   const int tid = threadIdx.x;
-  // up to two (l, j) pairs per thread (r <= 45 -> r^2 <= 2048)
   const int npair = r * r;
-  int l0 = 0, j0 = 0, l1 = 0, j1 = 0;
-  bool a0 = false, a1 = false;
-  if (tid < npair) {
-    l0 = tid % r;
-    j0 = tid / r;
-    a0 = l0 <= j0;
+  int pl[kPgPairs], pj[kPgPairs];
+  bool act[kPgPairs];
+  double acc[kPgPairs];
+#pragma unroll
+  for (int q = 0; q < kPgPairs; ++q) {
+    const int idx = tid + kPgThreads * q;
+    pl[q] = idx < npair ? idx % r : 0;
+    pj[q] = idx < npair ? idx / r : 0;
+    act[q] = idx < npair && pl[q] <= pj[q];
+    acc[q] = 0.0;
   }
-  if (tid + 1024 < npair) {
-    l1 = (tid + 1024) % r;
-    j1 = (tid + 1024) / r;
-    a1 = l1 <= j1;
-  }
-  double s0 = 0.0, s1 = 0.0;
   const long long ntiles = (n_d + kPgTile - 1) / kPgTile;
   auto load = [&](long long t, double* dst) {
     const long long i0 = t * kPgTile;
-    for (int e = tid; e < kPgTile * r; e += 1024) {
+    for (int e = tid; e < kPgTile * r; e += kPgThreads) {
       const int ii = e / r, c = e % r;
       dst[e] = (i0 + ii < n_d) ? left[(i0 + ii) * capr + c] : 0.0;
     }
@@ -893,44 +892,39 @@ __global__ void __launch_bounds__(1024) pgram_kernel(const Ctrl* ctrl, const dou
   if (ntiles > 0) load(0, tile);
   __syncthreads();
   for (long long t = 0; t < ntiles; ++t) {
-    double* cur = tile + (t & 1) * kPgTile * r;
+    const double* cur = tile + (t & 1) * kPgTile * r;
     if (t + 1 < ntiles) load(t + 1, tile + ((t + 1) & 1) * kPgTile * r);
-    if (a0) {
+#pragma unroll
+    for (int q = 0; q < kPgPairs; ++q) {
+      if (!act[q]) continue;
+      double sacc = acc[q];
 #pragma unroll 8
       for (int ii = 0; ii < kPgTile; ++ii) {
-        const double w = cur[ii * r + j0];
-        if (w != 0.0) s0 += cur[ii * r + l0] * w;
+        const double w = cur[ii * r + pj[q]];
+        if (w != 0.0) sacc += cur[ii * r + pl[q]] * w;
       }
-    }
-    if (a1) {
-#pragma unroll 8
-      for (int ii = 0; ii < kPgTile; ++ii) {
-        const double w = cur[ii * r + j1];
-        if (w != 0.0) s1 += cur[ii * r + l1] * w;
-      }
+      acc[q] = sacc;
     }
     __syncthreads();
   }
-  if (a0) {
-    pg[l0 + j0 * r] = s0;
-    pg[j0 + l0 * r] = s0;
-  }
-  if (a1) {
-    pg[l1 + j1 * r] = s1;
-    pg[j1 + l1 * r] = s1;
-  }
+#pragma unroll
+  for (int q = 0; q < kPgPairs; ++q)
+    if (act[q]) {
+      pg[pl[q] + pj[q] * r] = acc[q];
+      pg[pj[q] + pl[q] * r] = acc[q];
+    }
   // r > 45: the remaining pairs the slow way (not reached by the configs)
-  for (int idx = tid + 2048; idx < npair; idx += 1024) {
+  for (int idx = tid + kPgThreads * kPgPairs; idx < npair; idx += kPgThreads) {
     const int l = idx % r, j = idx / r;
     if (l > j) continue;
-    double s = 0.0;
+    double sacc = 0.0;
     for (long long i = 0; i < n_d; ++i) {
       const double w = left[i * capr + j];
       if (w == 0.0) continue;
-      s += left[i * capr + l] * w;
+      sacc += left[i * capr + l] * w;
     }
-    pg[l + j * r] = s;
-    pg[j + l * r] = s;
+    pg[l + j * r] = sacc;
+    pg[j + l * r] = sacc;
   }
 }
 
@@ -1539,8 +1533,8 @@ void launch_isvd(const IsvdBufs& B0, cudaStream_t st) {
     clive = true;
   }
   mark(0);
-  pgram_kernel<<<1, 1024, sizeof(double) * 2 * kPgTile * capr, st>>>(B.ctrl, B.left, capr,
-                                                                     B.inner + L.pg);
+  pgram_kernel<<<1, kPgThreads, sizeof(double) * 2 * kPgTile * capr, st>>>(B.ctrl, B.left, capr,
+                                                                           B.inner + L.pg);
   mark(1);
   isvd_pass1_kernel<<<nb, 256, 0, st>>>(B.ctrl, B.q, B.b, n, rows_per, capr, part1);
   mark(2);
