@@ -23,3 +23,25 @@ def test_reference_arm_json_line():
     assert d["impl"] == "reference" and d["steps"] == 3 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] == 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0
+
+
+def test_both_arms_share_config_and_slice_bytes():
+    """the reference arm and ours stream identical bytes and
+    report the same `config` object; priming (graph-cache setup of our engine)
+    is separate from the W warm-up updates and consumed by both arms."""
+    import argparse
+    import importlib.util
+    import numpy as np
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(ROOT, "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    from paper_2308_16395_b200 import datagen as dg
+    cfg = dg.CONFIGS["c2"]
+    args = argparse.Namespace(config="c2")
+    a = bench.base_config(args, cfg, "single")
+    b = bench.base_config(args, cfg, "single")
+    assert a == b and "numpy" in a["slice_source"] and a["n_slices"] == 100
+    assert "slice_torch" in bench.slice_source(dg.CONFIGS["c4"])   # multi-GB slices: device synthesis
+    small = dg.CONFIGS["c1"]
+    gen = dg.make_stream(small)
+    np.testing.assert_array_equal(bench.bench_slice_host(gen, small, 25), gen.slice_numpy(25))
